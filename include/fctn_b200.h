@@ -1,0 +1,137 @@
+/*
+ * fctn_b200.h — C ABI of the B200-native PAM sweep for trace-regularized
+ * FCTN tensor completion (arXiv 2510.22506).
+ *
+ * The reference (`fctnlr` 0.1.0, pure Python/numpy) has no FFI layer; its
+ * drop-in boundary is the Python solver API `fctnlr.solver.run(obs, cfg)`
+ * (solver.py:277).  These entry points are what that API's inner loop binds
+ * to (the ctypes binding lives in paper_2510_22506_b200/_native.py; see
+ * INTEGRATION.md for the stub a reference maintainer would add).  Every
+ * pointer is a plain host pointer; no torch types cross the boundary.
+ *
+ * Layout conventions (reference tensor.py:1-12): first-index-fastest.
+ *  - X, mask: order-N tensor, F-order, `dims` extents.
+ *  - factor k: its mode-k unfolding A_(k), an I_k x s_k column-major matrix
+ *    (rows mode k, columns the other slots ascending, first fastest) —
+ *    `mode_unfold(f.factor(k), k)` (solver.py:325, tensor.py:130-139).
+ *  - rank table: strict upper triangle, row-major (network.py:41-85).
+ *
+ * Status codes: 0 ok; 1 usage/shape error (-> ValueError); 2 numerical
+ * failure (-> NumericalFailure, sylvester.py:39-40,109-113, solver.py:304,357);
+ * 3 CUDA/runtime error.  `fctn_last_error` gives the message.
+ *
+ * Determinism: fixed reduction orders, no floating-point atomics; identical
+ * inputs give identical bits (test_acceptance.py:407-443 contract).
+ * A context owns all its device memory and one CUDA stream; not thread-safe.
+ */
+#ifndef FCTN_B200_H
+#define FCTN_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct fctn_ctx fctn_ctx;
+
+#define FCTN_F64 0
+#define FCTN_F32 1
+
+#define FCTN_ALG_PLAIN 0       /* algorithm="fctnlr"  (solver.py:322-324, 343) */
+#define FCTN_ALG_ACCEL 1       /* algorithm="afctnlr" (solver.py:318-320, 337-341) */
+
+#define FCTN_SIGN_PD 0         /* laplacian_sign="positive-definite" (laplacian.py:22) */
+#define FCTN_SIGN_PRINTED 1    /* laplacian_sign="as-printed" */
+
+/* Sweep statistics written by fctn_sweep (indices into `out`). */
+#define FCTN_ST_OBJECTIVE 0    /* objective after the sweep (solver.py:356) */
+#define FCTN_ST_DIFF_SQ 1      /* ||X_new - X_old||^2 (solver.py:346) */
+#define FCTN_ST_BASE_SQ 2      /* ||X_old||^2 (solver.py:347) */
+#define FCTN_ST_DATA_SQ 3      /* ||X_new - C||^2 (solver.py:220) */
+#define FCTN_ST_XNEW_SQ 4      /* ||X_new||^2 (solver.py:382) */
+#define FCTN_ST_PENALTY 5      /* sum_k lam_k/2 tr(A^T L A) (solver.py:221-223) */
+#define FCTN_ST_STEP_FAC 6     /* sum_k ||A_new - A_prev||^2 (solver.py:332) */
+#define FCTN_ST_FNORM_MAX 7    /* max_k ||A_k||_F (solver.py:383-385) */
+#define FCTN_ST_DEVICE_MS 8    /* CUDA-event time of the sweep */
+#define FCTN_ST_COUNT 16
+
+/* Trace counters written by fctn_sweep / fctn_plan_sweeps (indices). */
+#define FCTN_CT_FLOPS 0        /* reference FLOP meter total for the sweep (tensor.py:32-72) */
+#define FCTN_CT_MK 1           /* "mk" label */
+#define FCTN_CT_COMPOSE 2      /* "compose" label */
+#define FCTN_CT_HITS 3         /* reuse-cache hits (network.py:398-407) */
+#define FCTN_CT_LAUNCHES 4     /* kernels launched by the library in the sweep */
+#define FCTN_CT_COUNT 8
+
+/* Create a context on `device`.  Replaces the setup of solver.py:278-300:
+ * rank table (network.py:68-77), Laplacian spectra (laplacian.py:46-47), the
+ * reuse cache with its fp64 byte budget (network.py:377-417; solver.py:127).
+ * `lam`, `delta`: n values each.  `n_ranks`/`rank`: sharding along mode 0
+ * (slab [slab_lo, slab_hi) of I_0 held by this rank; pass 0,1,0,dims[0] for
+ * a single GPU). */
+int fctn_create(int device, int dtype, int n, const int64_t* dims, const int64_t* rank_tri,
+                const double* lam, const double* delta, int lap_sign, double rho, int algorithm,
+                int64_t cache_budget, fctn_ctx** out);
+
+/* Host -> device: the observed tensor (values zero off the mask; solver.py:79,297)
+ * in the context dtype (double* for FCTN_F64, float* for FCTN_F32) and the
+ * mask (one byte per entry, 0/1).  Sets X := values. */
+int fctn_upload(fctn_ctx* ctx, const void* x_F, const uint8_t* mask_F);
+
+/* Replace every factor (mode-k unfoldings, float64) and their version stamps
+ * (network.py:193-200; growth re-layout solver.py:365-367 resets the cache). */
+int fctn_set_factors(fctn_ctx* ctx, const double* const* a_unf, const int64_t* versions,
+                     int reset_cache);
+
+/* Change the rank table (rank growth, solver.py:361-368); factors must be set
+ * afterwards with fctn_set_factors. */
+int fctn_set_rank(fctn_ctx* ctx, const int64_t* rank_tri);
+
+/* Device -> host. */
+int fctn_get_factors(fctn_ctx* ctx, double* const* a_unf);
+int fctn_get_x(fctn_ctx* ctx, void* x_F);  /* context dtype, like fctn_upload */
+
+/* f(X, {A_k}) of solver.py:209-224 for the context's current X and factors
+ * (full composition; used for the initial objective solver.py:302 and the
+ * rank-growth continuity test solver.py:416).  Adds the compose FLOPs of the
+ * reference's chain `compose` (network.py:271-278) to counters[FCTN_CT_*]
+ * when counters != NULL. */
+int fctn_objective(fctn_ctx* ctx, double* out_objective, int64_t* counters);
+
+/* One PAM sweep (solver.py:307-359): N factor updates in `order` (merge of
+ * all factors but k with device-resident reuse cache, network.py:426-498;
+ * streaming products and exact subproblem solve, sylvester.py:51-116;
+ * optional extrapolation, solver.py:240-243,330-331), then compose from the
+ * last partial (network.py:313-332) fused with the P_Omega blend
+ * (solver.py:227-237) and the reductions.  `extrap`=0 disables extrapolation.
+ * `stats`: FCTN_ST_COUNT doubles; `counters`: FCTN_CT_COUNT int64. */
+int fctn_sweep(fctn_ctx* ctx, const int32_t* order, int extrap, double alpha, double beta,
+               double* stats, int64_t* counters);
+
+/* Shape-only replay (no device needed): the reference FLOP meter and cache
+ * hit counters for `n_sweeps` sweeps with the given visiting orders
+ * (n_sweeps x n int32), fixed rank.  `counters`: n_sweeps x FCTN_CT_COUNT. */
+int fctn_plan_sweeps(int n, const int64_t* dims, const int64_t* rank_tri, int algorithm,
+                     int64_t cache_budget, int n_sweeps, const int32_t* orders, int64_t* counters);
+
+/* Multi-GPU (one process per GPU, sharded along mode 0): an NCCL unique id
+ * (128 bytes) made on rank 0 and shared by the caller, then the communicator.
+ * Per factor update the rank-sized partial products are all-reduced
+ * (Y_k, G_k for k != 0; Y_0 rows all-gathered), per sweep 4 scalars. */
+int fctn_nccl_unique_id(uint8_t* id128);
+int fctn_set_comm(fctn_ctx* ctx, const uint8_t* id128, int rank, int nranks, int64_t slab_lo,
+                  int64_t slab_hi);
+
+/* Sync the context stream and return the device time of the last sweep. */
+int fctn_sync(fctn_ctx* ctx);
+
+const char* fctn_last_error(fctn_ctx* ctx);
+const char* fctn_version(void);
+void fctn_destroy(fctn_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* FCTN_B200_H */

@@ -1,0 +1,195 @@
+"""ctypes binding of libfctn_b200.so (the C ABI in include/fctn_b200.h).
+
+There is no fallback: if the library is missing or cannot be loaded the
+import of the device path raises.  Loading the library does not need a GPU;
+creating a context does.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libfctn_b200.so")
+
+F64, F32 = 0, 1
+ALG_PLAIN, ALG_ACCEL = 0, 1
+SIGN_PD, SIGN_PRINTED = 0, 1
+ST_OBJECTIVE, ST_DIFF_SQ, ST_BASE_SQ, ST_DATA_SQ, ST_XNEW_SQ = 0, 1, 2, 3, 4
+ST_PENALTY, ST_STEP_FAC, ST_FNORM_MAX, ST_DEVICE_MS, ST_COUNT = 5, 6, 7, 8, 16
+CT_FLOPS, CT_MK, CT_COMPOSE, CT_HITS, CT_LAUNCHES, CT_COUNT = 0, 1, 2, 3, 4, 8
+
+EXPORTS = [
+    "fctn_create", "fctn_upload", "fctn_set_factors", "fctn_set_rank", "fctn_get_factors", "fctn_get_x",
+    "fctn_objective", "fctn_sweep", "fctn_plan_sweeps", "fctn_nccl_unique_id", "fctn_set_comm",
+    "fctn_sync", "fctn_last_error", "fctn_version", "fctn_destroy",
+]
+
+_lib = None
+
+
+class NativeError(RuntimeError):
+    pass
+
+
+def lib():
+    """Load (once) and type the shared library; raises if it is absent."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: build it with `python -m paper_2510_22506_b200.build` "
+                          "(there is no CPU fallback)")
+    L = C.CDLL(LIB_PATH)
+    P = C.c_void_p
+    i64p = C.POINTER(C.c_int64)
+    f64p = C.POINTER(C.c_double)
+    L.fctn_create.argtypes = [C.c_int, C.c_int, C.c_int, i64p, i64p, f64p, f64p, C.c_int, C.c_double, C.c_int,
+                              C.c_int64, C.POINTER(P)]
+    L.fctn_upload.argtypes = [P, P, P]
+    L.fctn_set_factors.argtypes = [P, C.POINTER(P), i64p, C.c_int]
+    L.fctn_set_rank.argtypes = [P, i64p]
+    L.fctn_get_factors.argtypes = [P, C.POINTER(P)]
+    L.fctn_get_x.argtypes = [P, P]
+    L.fctn_objective.argtypes = [P, f64p, i64p]
+    L.fctn_sweep.argtypes = [P, C.POINTER(C.c_int32), C.c_int, C.c_double, C.c_double, f64p, i64p]
+    L.fctn_plan_sweeps.argtypes = [C.c_int, i64p, i64p, C.c_int, C.c_int64, C.c_int, C.POINTER(C.c_int32), i64p]
+    L.fctn_nccl_unique_id.argtypes = [P]
+    L.fctn_set_comm.argtypes = [P, P, C.c_int, C.c_int, C.c_int64, C.c_int64]
+    L.fctn_sync.argtypes = [P]
+    L.fctn_last_error.argtypes = [P]
+    L.fctn_last_error.restype = C.c_char_p
+    L.fctn_version.argtypes = []
+    L.fctn_version.restype = C.c_char_p
+    L.fctn_destroy.argtypes = [P]
+    L.fctn_destroy.restype = None
+    for name in EXPORTS:
+        if not hasattr(L, name):
+            raise ImportError(f"{LIB_PATH} does not export {name}")
+    _lib = L
+    return L
+
+
+def _i64(a):
+    a = np.ascontiguousarray(np.asarray(a, dtype=np.int64))
+    return a, a.ctypes.data_as(C.POINTER(C.c_int64))
+
+
+def _f64(a):
+    a = np.ascontiguousarray(np.asarray(a, dtype=np.float64))
+    return a, a.ctypes.data_as(C.POINTER(C.c_double))
+
+
+def check(rc: int, handle=None, numeric_exc=None):
+    if rc == 0:
+        return
+    msg = lib().fctn_last_error(handle).decode()
+    if rc == 1:
+        raise ValueError(msg)
+    if rc == 2:
+        raise (numeric_exc or NativeError)(msg)
+    raise NativeError(msg)
+
+
+def plan_sweeps(dims, rank_tri, algorithm: int, cache_budget: int, orders) -> np.ndarray:
+    """Shape-only replay of the reference FLOP meter and cache hits."""
+    orders = np.ascontiguousarray(np.asarray(orders, dtype=np.int32))
+    n = len(dims)
+    ns = orders.shape[0]
+    d, dp = _i64(dims)
+    r, rp = _i64(rank_tri)
+    out = np.zeros((ns, CT_COUNT), dtype=np.int64)
+    rc = lib().fctn_plan_sweeps(n, dp, rp, algorithm, int(cache_budget), ns,
+                                orders.ctypes.data_as(C.POINTER(C.c_int32)),
+                                out.ctypes.data_as(C.POINTER(C.c_int64)))
+    check(rc)
+    return out
+
+
+class Context:
+    """Owns one device context (one GPU, one CUDA stream)."""
+
+    def __init__(self, device, dtype: int, dims, rank_tri, lams, deltas, sign: int, rho: float,
+                 algorithm: int, cache_budget: int, numeric_exc=None):
+        self._numeric = numeric_exc
+        L = lib()
+        self.dims = tuple(int(d) for d in dims)
+        self.n = len(self.dims)
+        self.dtype = dtype
+        self.np_dtype = np.float64 if dtype == F64 else np.float32
+        d, dp = _i64(self.dims)
+        r, rp = _i64(rank_tri)
+        lm, lp = _f64(lams)
+        dl, dlp = _f64(deltas)
+        h = C.c_void_p()
+        rc = L.fctn_create(int(device), dtype, self.n, dp, rp, lp, dlp, sign, float(rho), algorithm,
+                           int(cache_budget), C.byref(h))
+        if rc:
+            msg = L.fctn_last_error(None).decode()
+            if rc == 1:
+                raise ValueError(msg)
+            raise NativeError(msg)
+        self.h = h
+        self.rank_tri = tuple(int(v) for v in rank_tri)
+        self._stats = np.zeros(ST_COUNT, dtype=np.float64)
+        self._counters = np.zeros(CT_COUNT, dtype=np.int64)
+
+    def _check(self, rc):
+        check(rc, self.h, self._numeric)
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().fctn_destroy(self.h)
+            self.h = None
+
+    def __del__(self):  # pragma: no cover
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def upload(self, values: np.ndarray, mask: np.ndarray):
+        x = np.asfortranarray(values, dtype=self.np_dtype)
+        m = np.asfortranarray(mask, dtype=np.uint8)
+        self._check(lib().fctn_upload(self.h, x.ctypes.data_as(C.c_void_p), m.ctypes.data_as(C.c_void_p)))
+
+    def set_rank(self, rank_tri):
+        r, rp = _i64(rank_tri)
+        self._check(lib().fctn_set_rank(self.h, rp))
+        self.rank_tri = tuple(int(v) for v in rank_tri)
+
+    def set_factors(self, unfoldings, versions, reset_cache: bool):
+        arrs = [np.asfortranarray(a, dtype=np.float64) for a in unfoldings]
+        ptrs = (C.c_void_p * self.n)(*[a.ctypes.data for a in arrs])
+        v, vp = _i64(versions)
+        self._check(lib().fctn_set_factors(self.h, ptrs, vp, int(bool(reset_cache))))
+
+    def get_factors(self, shapes):
+        arrs = [np.empty(s, dtype=np.float64, order="F") for s in shapes]
+        ptrs = (C.c_void_p * self.n)(*[a.ctypes.data for a in arrs])
+        self._check(lib().fctn_get_factors(self.h, ptrs))
+        return arrs
+
+    def get_x(self) -> np.ndarray:
+        out = np.empty(self.dims, dtype=self.np_dtype, order="F")
+        self._check(lib().fctn_get_x(self.h, out.ctypes.data_as(C.c_void_p)))
+        return out
+
+    def objective(self):
+        v = C.c_double()
+        ct = np.zeros(CT_COUNT, dtype=np.int64)
+        self._check(lib().fctn_objective(self.h, C.byref(v), ct.ctypes.data_as(C.POINTER(C.c_int64))))
+        return float(v.value), ct
+
+    def sweep(self, order, extrapolation=None):
+        o = np.ascontiguousarray(np.asarray(order, dtype=np.int32))
+        ex, a, b = (0, 0.0, 0.0) if extrapolation is None else (1, float(extrapolation[0]), float(extrapolation[1]))
+        self._check(lib().fctn_sweep(self.h, o.ctypes.data_as(C.POINTER(C.c_int32)), ex, a, b,
+                                     self._stats.ctypes.data_as(C.POINTER(C.c_double)),
+                                     self._counters.ctypes.data_as(C.POINTER(C.c_int64))))
+        return self._stats.copy(), self._counters.copy()
+
+    def sync(self):
+        self._check(lib().fctn_sync(self.h))

@@ -1,0 +1,758 @@
+// Context, device executor and the C ABI (include/fctn_b200.h).
+//
+// The context owns X (double-buffered), the mask, the factors (fp64 master
+// + compute-dtype copy), the M_k buffer, the reuse-cache allocations and the
+// small solve workspaces.  One sweep = one host call; the host sees only the
+// few sweep scalars copied back at the end (solver.py:346-388 needs them).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/fctn_b200.h"
+#include "executor.hpp"
+#include "kernels.cuh"
+#include "plan.hpp"
+
+namespace fctn {
+
+struct UsageError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct NumericError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct CudaError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+#define CK(call)                                                                             \
+  do {                                                                                       \
+    cudaError_t _e = (call);                                                                 \
+    if (_e != cudaSuccess)                                                                   \
+      throw ::fctn::CudaError(std::string(#call) + " failed: " + cudaGetErrorString(_e));            \
+  } while (0)
+
+struct Tables {
+  int64_t* d = nullptr;  // rowA | rowC | colB | colC | kA | kB
+  int64_t rows = 0, cols = 0, K = 0;
+  bool swap = false;
+};
+
+static const int64_t M_ID = 0;  // fixed executor id of the M_k buffer
+
+class Ctx : public Executor {
+ public:
+  int device = 0;
+  int dtype = FCTN_F64;
+  size_t esize = 8;
+  Shape sh;
+  std::vector<double> lam, delta;
+  int sign = FCTN_SIGN_PD;
+  double rho = 0.1;
+  int alg = FCTN_ALG_ACCEL;
+  int64_t budget = 1 << 30;
+  std::string err;
+  cudaStream_t st = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  std::unique_ptr<Planner> planner;
+  int64_t launches = 0;
+
+  // device memory
+  std::map<int64_t, void*> bufs;
+  int64_t next_id = 1;
+  void* X[2] = {nullptr, nullptr};
+  int cur = 0;
+  uint8_t* mask = nullptr;
+  std::vector<double*> A64;
+  std::vector<void*> Ac;  // compute copy (== A64 for fp64)
+  double* Ascratch = nullptr;
+  void* Mbuf = nullptr;
+  double *Y = nullptr, *G = nullptr, *Fr = nullptr, *Fi = nullptr;
+  double *ypart = nullptr, *gpart = nullptr;
+  double* partials = nullptr;
+  int64_t partial_cap = 0;
+  std::vector<double*> mu, cosT, sinT;
+  std::vector<double> check_mu;
+  double* dstats = nullptr;  // [n*3 factor stats][4 sums]
+  int* dstatus = nullptr;
+  double* hstats = nullptr;  // pinned mirror (+ status)
+  std::map<std::string, Tables> tables;
+  bool configured = false;
+  bool uploaded = false;
+
+  ~Ctx() override { release_all(); }
+
+  // ------------------------------------------------------------ executor
+  int64_t alloc(int64_t numel) override {
+    void* p = nullptr;
+    CK(cudaMallocAsync(&p, std::max<int64_t>(numel, 1) * esize, st));
+    int64_t id = next_id++;
+    bufs[id] = p;
+    return id;
+  }
+  void free(int64_t id) override {
+    if (id == M_ID) return;
+    auto it = bufs.find(id);
+    if (it == bufs.end()) return;
+    CK(cudaFreeAsync(it->second, st));
+    bufs.erase(it);
+  }
+  bool is_fixed_buffer(int64_t id) const override { return id == M_ID; }
+
+  void* ptr_of(const LTensor& t) {
+    if (t.factor >= 0) return Ac[t.factor];
+    if (t.buf == M_ID) return Mbuf;
+    auto it = bufs.find(t.buf);
+    if (it == bufs.end()) throw std::runtime_error("unknown buffer id");
+    return it->second;
+  }
+
+  std::vector<int64_t> strides_of(const std::vector<int>& labels) const {
+    std::vector<int64_t> s(labels.size());
+    int64_t acc = 1;
+    for (size_t i = 0; i < labels.size(); ++i) {
+      s[i] = acc;
+      acc *= sh.extent(labels[i]);
+    }
+    return s;
+  }
+  static int64_t stride_in(const std::vector<int>& labels, const std::vector<int64_t>& strides, int l) {
+    for (size_t i = 0; i < labels.size(); ++i)
+      if (labels[i] == l) return strides[i];
+    throw std::runtime_error("label not found");
+  }
+
+  // offsets of a mixed-radix enumeration over `labs` (first fastest)
+  void enum_offsets(const std::vector<int>& labs, const std::vector<int>& l1, const std::vector<int64_t>& s1,
+                    const std::vector<int>& l2, const std::vector<int64_t>& s2, std::vector<int64_t>& o1,
+                    std::vector<int64_t>& o2) {
+    int64_t cnt = 1;
+    std::vector<int64_t> ext, st1, st2;
+    for (int l : labs) {
+      ext.push_back(sh.extent(l));
+      st1.push_back(stride_in(l1, s1, l));
+      st2.push_back(stride_in(l2, s2, l));
+      cnt *= sh.extent(l);
+    }
+    o1.resize(cnt);
+    o2.resize(cnt);
+    std::vector<int64_t> dig(labs.size(), 0);
+    int64_t a = 0, b = 0;
+    for (int64_t e = 0; e < cnt; ++e) {
+      o1[e] = a;
+      o2[e] = b;
+      for (size_t q = 0; q < labs.size(); ++q) {
+        ++dig[q];
+        a += st1[q];
+        b += st2[q];
+        if (dig[q] < ext[q]) break;
+        a -= st1[q] * ext[q];
+        b -= st2[q] * ext[q];
+        dig[q] = 0;
+      }
+    }
+  }
+
+  static std::string key_of(const ContractOp& op) {
+    std::string k;
+    auto add = [&](const std::vector<int>& v) {
+      for (int x : v) k += std::to_string(x) + ",";
+      k += "|";
+    };
+    add(op.a.labels);
+    add(op.b.labels);
+    add(op.out.labels);
+    return k;
+  }
+
+  Tables& tables_for(const ContractOp& op) {
+    std::string key = key_of(op);
+    auto it = tables.find(key);
+    if (it != tables.end()) return it->second;
+    const std::vector<int>& out = op.out.labels;
+    std::vector<int64_t> so = strides_of(out);
+    bool fast_in_b = std::find(op.b.labels.begin(), op.b.labels.end(), out[0]) != op.b.labels.end();
+    const LTensor& ra = fast_in_b ? op.b : op.a;  // "row" operand
+    const LTensor& cb = fast_in_b ? op.a : op.b;
+    std::vector<int64_t> sa = strides_of(ra.labels), sb = strides_of(cb.labels);
+    std::vector<int> rfree, cfree, shared;
+    for (int l : ra.labels) {
+      if (std::find(cb.labels.begin(), cb.labels.end(), l) != cb.labels.end())
+        shared.push_back(l);
+      else
+        rfree.push_back(l);
+    }
+    for (int l : cb.labels)
+      if (std::find(ra.labels.begin(), ra.labels.end(), l) == ra.labels.end()) cfree.push_back(l);
+    auto by_out_stride = [&](std::vector<int>& v) {
+      std::sort(v.begin(), v.end(),
+                [&](int x, int y) { return stride_in(out, so, x) < stride_in(out, so, y); });
+    };
+    by_out_stride(rfree);
+    by_out_stride(cfree);
+    std::vector<int64_t> rowA, rowC, colB, colC, kA, kB;
+    enum_offsets(rfree, ra.labels, sa, out, so, rowA, rowC);
+    enum_offsets(cfree, cb.labels, sb, out, so, colB, colC);
+    enum_offsets(shared, ra.labels, sa, cb.labels, sb, kA, kB);
+    Tables t;
+    t.rows = (int64_t)rowA.size();
+    t.cols = (int64_t)colB.size();
+    t.K = (int64_t)kA.size();
+    t.swap = fast_in_b;
+    int64_t total = 2 * t.rows + 2 * t.cols + 2 * t.K;
+    std::vector<int64_t> h;
+    h.reserve(total);
+    h.insert(h.end(), rowA.begin(), rowA.end());
+    h.insert(h.end(), rowC.begin(), rowC.end());
+    h.insert(h.end(), colB.begin(), colB.end());
+    h.insert(h.end(), colC.begin(), colC.end());
+    h.insert(h.end(), kA.begin(), kA.end());
+    h.insert(h.end(), kB.begin(), kB.end());
+    CK(cudaMalloc(&t.d, total * sizeof(int64_t)));
+    CK(cudaMemcpyAsync(t.d, h.data(), total * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+    CK(cudaStreamSynchronize(st));  // host vector goes out of scope
+    return tables.emplace(key, t).first->second;
+  }
+
+  void contract(const ContractOp& op) override {
+    Tables& t = tables_for(op);
+    const void* ra = ptr_of(t.swap ? op.b : op.a);
+    const void* cb = ptr_of(t.swap ? op.a : op.b);
+    void* out = ptr_of(op.out);
+    const int64_t* d = t.d;
+    const int64_t *rowA = d, *rowC = d + t.rows, *colB = d + 2 * t.rows, *colC = d + 2 * t.rows + t.cols;
+    const int64_t *kA = d + 2 * t.rows + 2 * t.cols, *kB = kA + t.K;
+    if (dtype == FCTN_F64)
+      launch_contract<double>((const double*)ra, (const double*)cb, (double*)out, rowA, rowC, colB, colC, kA, kB,
+                              t.rows, t.cols, t.K, st);
+    else
+      launch_contract<float>((const float*)ra, (const float*)cb, (float*)out, rowA, rowC, colB, colC, kA, kB,
+                             t.rows, t.cols, t.K, st);
+    ++launches;
+  }
+
+  void permute(const LTensor& in, const LTensor& out) override {
+    PermDesc pd;
+    pd.nd = (int)out.labels.size();
+    if (pd.nd > 16) throw std::runtime_error("too many modes");
+    std::vector<int64_t> si = strides_of(in.labels);
+    int64_t numel = 1;
+    for (int q = 0; q < pd.nd; ++q) {
+      pd.ext[q] = sh.extent(out.labels[q]);
+      pd.in_stride[q] = stride_in(in.labels, si, out.labels[q]);
+      numel *= pd.ext[q];
+    }
+    if (dtype == FCTN_F64)
+      launch_permute<double>((const double*)ptr_of(in), (double*)ptr_of(out), pd, numel, st);
+    else
+      launch_permute<float>((const float*)ptr_of(in), (float*)ptr_of(out), pd, numel, st);
+    ++launches;
+  }
+
+  // ------------------------------------------------------------ setup
+  void release_shape_buffers() {
+    for (auto& kv : bufs) cudaFree(kv.second);
+    bufs.clear();
+    for (auto& kv : tables) cudaFree(kv.second.d);
+    tables.clear();
+    for (size_t k = 0; k < A64.size(); ++k) {
+      cudaFree(A64[k]);
+      if (dtype == FCTN_F32) cudaFree(Ac[k]);
+    }
+    A64.clear();
+    Ac.clear();
+    for (auto* p : {Ascratch, (double*)Mbuf, Y, G, Fr, Fi, ypart, gpart, partials}) cudaFree(p);
+    Ascratch = nullptr;
+    Mbuf = nullptr;
+    Y = G = Fr = Fi = ypart = gpart = partials = nullptr;
+  }
+  void release_all() {
+    if (st) cudaStreamSynchronize(st);
+    release_shape_buffers();
+    for (auto* p : mu) cudaFree(p);
+    for (auto* p : cosT) cudaFree(p);
+    for (auto* p : sinT) cudaFree(p);
+    mu.clear();
+    cosT.clear();
+    sinT.clear();
+    cudaFree(X[0]);
+    cudaFree(X[1]);
+    cudaFree(mask);
+    cudaFree(dstats);
+    cudaFree(dstatus);
+    if (hstats) cudaFreeHost(hstats);
+    X[0] = X[1] = nullptr;
+    mask = nullptr;
+    dstats = nullptr;
+    dstatus = nullptr;
+    hstats = nullptr;
+    if (ev0) cudaEventDestroy(ev0);
+    if (ev1) cudaEventDestroy(ev1);
+    if (st) cudaStreamDestroy(st);
+    ev0 = ev1 = nullptr;
+    st = nullptr;
+  }
+
+  int target_ctas() const { return 148 * 8; }
+
+  void configure_shape() {
+    // (re)allocate everything whose size depends on the rank table
+    release_shape_buffers();
+    const int n = sh.n;
+    const int64_t T = sh.total();
+    int64_t max_is = 1, max_ss = 1, max_m = 1, max_h = 1, max_yp = 1, max_gp = 1, max_part = 1;
+    for (int k = 0; k < n; ++k) {
+      int64_t I = sh.dims[k], S = sh.s_of(k), p = T / I;
+      max_is = std::max(max_is, I * S);
+      max_ss = std::max(max_ss, S * S);
+      max_m = std::max(max_m, S * p);
+      max_h = std::max(max_h, (I / 2 + 1) * S);
+      StreamPlan sy = plan_stream(I, S, p, target_ctas());
+      StreamPlan sg = plan_stream(S, S, p, target_ctas());
+      max_yp = std::max(max_yp, (int64_t)sy.nsplit * I * S);
+      max_gp = std::max(max_gp, (int64_t)sg.nsplit * S * S);
+      max_part = std::max(max_part, ((I + 63) / 64) * ((p + 63) / 64));
+    }
+    A64.assign(n, nullptr);
+    Ac.assign(n, nullptr);
+    for (int k = 0; k < n; ++k) {
+      int64_t e = sh.dims[k] * sh.s_of(k);
+      CK(cudaMalloc(&A64[k], e * sizeof(double)));
+      CK(cudaMemset(A64[k], 0, e * sizeof(double)));
+      if (dtype == FCTN_F32) {
+        CK(cudaMalloc(&Ac[k], e * sizeof(float)));
+      } else {
+        Ac[k] = A64[k];
+      }
+    }
+    CK(cudaMalloc(&Ascratch, max_is * sizeof(double)));
+    CK(cudaMalloc(&Mbuf, max_m * esize));
+    CK(cudaMalloc(&Y, max_is * sizeof(double)));
+    CK(cudaMalloc(&G, max_ss * sizeof(double)));
+    CK(cudaMalloc(&Fr, max_h * sizeof(double)));
+    CK(cudaMalloc(&Fi, max_h * sizeof(double)));
+    CK(cudaMalloc(&ypart, max_yp * sizeof(double)));
+    CK(cudaMalloc(&gpart, max_gp * sizeof(double)));
+    partial_cap = max_part;
+    CK(cudaMalloc(&partials, max_part * 4 * sizeof(double)));
+    std::vector<int64_t> versions = planner ? planner->versions : std::vector<int64_t>(n, 0);
+    planner.reset(new Planner(sh, budget));
+    planner->versions = versions;
+  }
+
+  void configure(int dev, int dt, int n, const int64_t* dims, const int64_t* tri, const double* lm,
+                 const double* dl, int sg, double r, int a, int64_t bud) {
+    if (n < 2) throw UsageError("need a tensor of order >= 2");
+    if (dt != FCTN_F64 && dt != FCTN_F32) throw UsageError("dtype must be FCTN_F64 or FCTN_F32");
+    if (!(r > 0.0)) throw UsageError("rho must be > 0");
+    device = dev;
+    dtype = dt;
+    esize = dt == FCTN_F64 ? 8 : 4;
+    sh.n = n;
+    sh.dims.assign(dims, dims + n);
+    sh.tri.assign(tri, tri + n * (n - 1) / 2);
+    for (auto d : sh.dims)
+      if (d < 1) throw UsageError("extents must be >= 1");
+    for (auto t : sh.tri)
+      if (t < 1) throw UsageError("rank entries must be >= 1");
+    lam.assign(lm, lm + n);
+    delta.assign(dl, dl + n);
+    for (int k = 0; k < n; ++k) {
+      if (lam[k] < 0) throw UsageError("lam must be >= 0");
+      if (!(delta[k] > 0)) throw UsageError("diagonal shift delta must be > 0");
+    }
+    sign = sg;
+    rho = r;
+    alg = a;
+    budget = bud;
+    CK(cudaSetDevice(device));
+    CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    CK(cudaEventCreate(&ev0));
+    CK(cudaEventCreate(&ev1));
+    {
+      cudaMemPool_t pool;
+      CK(cudaDeviceGetDefaultMemPool(&pool, device));
+      uint64_t thr = UINT64_MAX;
+      CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+    }
+    const int64_t T = sh.total();
+    CK(cudaMalloc(&X[0], T * esize));
+    CK(cudaMalloc(&X[1], T * esize));
+    CK(cudaMalloc(&mask, T));
+    CK(cudaMalloc(&dstats, (n * 3 + 8) * sizeof(double)));
+    CK(cudaMalloc(&dstatus, sizeof(int)));
+    CK(cudaMemset(dstatus, 0, sizeof(int)));
+    CK(cudaMallocHost(&hstats, (n * 3 + 8) * sizeof(double) + 64));
+    // spectra and DFT tables per mode (laplacian.py:46-47)
+    const double sgn = sign == FCTN_SIGN_PD ? -1.0 : 1.0;
+    mu.assign(n, nullptr);
+    cosT.assign(n, nullptr);
+    sinT.assign(n, nullptr);
+    check_mu.assign(n, NAN);
+    for (int k = 0; k < n; ++k) {
+      int64_t I = sh.dims[k];
+      std::vector<double> c(I), s(I), m(I / 2 + 1);
+      double lmin = INFINITY;
+      for (int64_t j = 0; j < I; ++j) {
+        double th = 2.0 * M_PI * (double)j / (double)I;
+        c[j] = std::cos(th);
+        s[j] = std::sin(th);
+        double L = sgn * (-2.0 - delta[k] + 2.0 * std::cos(th));
+        lmin = std::min(lmin, L);
+        if (j <= I / 2) m[j] = lam[k] * L + rho;
+      }
+      // T-floor guard (sylvester.py:108-113): min T = lam*min(Lambda) + phi_min + rho.
+      // It can only fail when lam*min(Lambda) + rho <= 1e-10 (phi >= 0 after the clamp).
+      double shift = lam[k] * lmin + rho - 1e-10;
+      if (shift <= 0.0) check_mu[k] = shift;
+      CK(cudaMalloc(&mu[k], m.size() * sizeof(double)));
+      CK(cudaMalloc(&cosT[k], I * sizeof(double)));
+      CK(cudaMalloc(&sinT[k], I * sizeof(double)));
+      CK(cudaMemcpy(mu[k], m.data(), m.size() * sizeof(double), cudaMemcpyHostToDevice));
+      CK(cudaMemcpy(cosT[k], c.data(), I * sizeof(double), cudaMemcpyHostToDevice));
+      CK(cudaMemcpy(sinT[k], s.data(), I * sizeof(double), cudaMemcpyHostToDevice));
+    }
+    configure_shape();
+    configured = true;
+  }
+
+  // ------------------------------------------------------------ sweep pieces
+  void factor_update(int k, int extrap, double alpha, double beta) {
+    const int64_t T = sh.total();
+    const int64_t I = sh.dims[k], S = sh.s_of(k), p = T / I;
+    int64_t P = 1;
+    for (int j = 0; j < k; ++j) P *= sh.dims[j];
+    StreamPlan sy = plan_stream(I, S, p, target_ctas());
+    StreamPlan sg = plan_stream(S, S, p, target_ctas());
+    if (dtype == FCTN_F64) {
+      launch_stream<double>((const double*)X[cur], (const double*)Mbuf, ypart, I, P, S, p, sy, st);
+      launch_stream<double>((const double*)Mbuf, (const double*)Mbuf, gpart, S, 1, S, p, sg, st);
+    } else {
+      launch_stream<float>((const float*)X[cur], (const float*)Mbuf, ypart, I, P, S, p, sy, st);
+      launch_stream<float>((const float*)Mbuf, (const float*)Mbuf, gpart, S, 1, S, p, sg, st);
+    }
+    launch_reduce_y(ypart, sy.nsplit, I, S, A64[k], rho, Y, st);
+    launch_reduce_g(gpart, sg.nsplit, S, G, st);
+    planner->meter.proj += 2 * I * p * S;   // sylvester.py:105
+    planner->meter.gram += 2 * S * S * p;   // sylvester.py:58
+    const int64_t H1 = I / 2 + 1;
+    launch_dft_fwd(Y, I, S, cosT[k], sinT[k], Fr, Fi, st);
+    launch_chol_solve(G, S, H1, mu[k], Fr, Fi, check_mu[k], dstatus, st);
+    if (dtype == FCTN_F64)
+      launch_dft_inv<double>(Fr, Fi, I, S, cosT[k], sinT[k], A64[k], Ascratch, nullptr, extrap, alpha, beta, st);
+    else
+      launch_dft_inv<float>(Fr, Fi, I, S, cosT[k], sinT[k], A64[k], Ascratch, (float*)Ac[k], extrap, alpha, beta,
+                            st);
+    const double sgn = sign == FCTN_SIGN_PD ? -1.0 : 1.0;
+    launch_factor_stats(Ascratch, A64[k], I, S, delta[k], sgn, dstats + 3 * k, st);
+    std::swap(A64[k], Ascratch);
+    if (dtype == FCTN_F64) Ac[k] = A64[k];
+    launches += 9;
+    planner->versions[k] += 1;  // network.py:200
+  }
+
+  void compose(int k, bool objective_only) {
+    const int64_t T = sh.total();
+    const int64_t I = sh.dims[k], S = sh.s_of(k), p = T / I;
+    int64_t P = 1;
+    for (int j = 0; j < k; ++j) P *= sh.dims[j];
+    int nb;
+    if (dtype == FCTN_F64)
+      nb = launch_compose<double>((const double*)Ac[k], (const double*)Mbuf, (const double*)X[cur], mask,
+                                  (double*)X[cur ^ 1], I, P, S, p, rho, objective_only, partials, partial_cap, st);
+    else
+      nb = launch_compose<float>((const float*)Ac[k], (const float*)Mbuf, (const float*)X[cur], mask,
+                                 (float*)X[cur ^ 1], I, P, S, p, rho, objective_only, partials, partial_cap, st);
+    launch_reduce4(partials, nb, dstats + 3 * sh.n, st);
+    launches += 2;
+  }
+
+  void fetch_stats() {
+    const int n = sh.n;
+    CK(cudaMemcpyAsync(hstats, dstats, (n * 3 + 4) * sizeof(double), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync((char*)(hstats + n * 3 + 8), dstatus, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    int status;
+    std::memcpy(&status, (char*)(hstats + n * 3 + 8), sizeof(int));
+    if (status) {
+      CK(cudaMemsetAsync(dstatus, 0, sizeof(int), st));
+      CK(cudaStreamSynchronize(st));
+      if (status & 1)
+        throw NumericError(
+            "shifted spectrum is not strictly positive; the as-printed operator orientation cannot be "
+            "inverted here");
+      throw NumericError("factor subproblem matrix is not positive definite (non-finite iterate)");
+    }
+  }
+
+  void sweep(const int32_t* order_in, int extrap, double alpha, double beta, double* stats, int64_t* counters) {
+    if (!uploaded) throw UsageError("no data uploaded");
+    const int n = sh.n;
+    std::vector<int> order(order_in, order_in + n);
+    {
+      std::vector<int> chk = order;
+      std::sort(chk.begin(), chk.end());
+      for (int i = 0; i < n; ++i)
+        if (chk[i] != i) throw UsageError("order is not a permutation of range(n)");
+    }
+    Meter m0 = planner->meter;
+    int64_t hits0 = planner->cache().hits;
+    launches = 0;
+    CK(cudaEventRecord(ev0, st));
+    for (int k : order) {
+      if (alg == FCTN_ALG_ACCEL)
+        planner->partial_cached(k, order, this, M_ID);
+      else
+        planner->partial_plain(k, this, M_ID);
+      factor_update(k, extrap, alpha, beta);
+    }
+    int k_last = order.back();
+    if (alg == FCTN_ALG_ACCEL) {
+      planner->meter.compose += 2 * (sh.total() / sh.dims[k_last]) * sh.s_of(k_last) * sh.dims[k_last];
+      compose(k_last, false);
+    } else {
+      // compose(f): the chain's FLOPs (network.py:271-278); on device the full
+      // tensor is A_(n-1) times the plain partial around n-1.
+      Meter keep = planner->meter;
+      planner->partial_plain(n - 1, this, M_ID);
+      planner->meter = keep;
+      planner->meter.compose += planner->compose_chain_flops();
+      compose(n - 1, false);
+    }
+    CK(cudaEventRecord(ev1, st));
+    fetch_stats();
+    cur ^= 1;
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, ev0, ev1));
+    double pen = 0.0, step = 0.0, fmax = 0.0;
+    for (int k = 0; k < n; ++k) {
+      step += hstats[3 * k + 0];
+      fmax = std::max(fmax, std::sqrt(hstats[3 * k + 1]));
+      pen += 0.5 * lam[k] * hstats[3 * k + 2];
+    }
+    const double* sums = hstats + 3 * n;
+    for (int i = 0; i < FCTN_ST_COUNT; ++i) stats[i] = 0.0;
+    stats[FCTN_ST_DIFF_SQ] = sums[0];
+    stats[FCTN_ST_BASE_SQ] = sums[1];
+    stats[FCTN_ST_DATA_SQ] = sums[2];
+    stats[FCTN_ST_XNEW_SQ] = sums[3];
+    stats[FCTN_ST_PENALTY] = pen;
+    stats[FCTN_ST_STEP_FAC] = step;
+    stats[FCTN_ST_FNORM_MAX] = fmax;
+    stats[FCTN_ST_OBJECTIVE] = 0.5 * sums[2] + pen;
+    stats[FCTN_ST_DEVICE_MS] = ms;
+    if (counters) {
+      for (int i = 0; i < FCTN_CT_COUNT; ++i) counters[i] = 0;
+      const Meter& m1 = planner->meter;
+      counters[FCTN_CT_FLOPS] = m1.total() - m0.total();
+      counters[FCTN_CT_MK] = m1.mk - m0.mk;
+      counters[FCTN_CT_COMPOSE] = m1.compose - m0.compose;
+      counters[FCTN_CT_HITS] = planner->cache().hits - hits0;
+      counters[FCTN_CT_LAUNCHES] = launches;
+    }
+  }
+
+  double objective(int64_t* counters) {
+    if (!uploaded) throw UsageError("no data uploaded");
+    const int n = sh.n;
+    Meter keep = planner->meter;
+    planner->partial_plain(0, this, M_ID);
+    planner->meter = keep;
+    compose(0, true);
+    const double sgn = sign == FCTN_SIGN_PD ? -1.0 : 1.0;
+    for (int k = 0; k < n; ++k)
+      launch_factor_stats(A64[k], A64[k], sh.dims[k], sh.s_of(k), delta[k], sgn, dstats + 3 * k, st);
+    fetch_stats();
+    double val = 0.5 * hstats[3 * n + 2];
+    for (int k = 0; k < n; ++k) val += 0.5 * lam[k] * hstats[3 * k + 2];
+    if (counters) {
+      for (int i = 0; i < FCTN_CT_COUNT; ++i) counters[i] = 0;
+      int64_t c = planner->compose_chain_flops();
+      counters[FCTN_CT_FLOPS] = c;
+      counters[FCTN_CT_COMPOSE] = c;
+    }
+    return val;
+  }
+};
+
+static thread_local std::string g_err;
+
+template <typename F>
+static int guarded(Ctx* c, F&& f) {
+  try {
+    f();
+    return 0;
+  } catch (const UsageError& e) {
+    (c ? c->err : g_err) = e.what();
+    return 1;
+  } catch (const NumericError& e) {
+    (c ? c->err : g_err) = e.what();
+    return 2;
+  } catch (const std::exception& e) {
+    (c ? c->err : g_err) = e.what();
+    return 3;
+  }
+}
+
+}  // namespace fctn
+
+using fctn::Ctx;
+
+struct fctn_ctx {
+  Ctx impl;
+};
+
+extern "C" {
+
+int fctn_create(int device, int dtype, int n, const int64_t* dims, const int64_t* rank_tri, const double* lam,
+                const double* delta, int lap_sign, double rho, int algorithm, int64_t cache_budget, fctn_ctx** out) {
+  *out = nullptr;
+  fctn_ctx* c = new fctn_ctx();
+  int rc = fctn::guarded(nullptr, [&] {
+    c->impl.configure(device, dtype, n, dims, rank_tri, lam, delta, lap_sign, rho, algorithm, cache_budget);
+  });
+  if (rc) {
+    delete c;
+    return rc;
+  }
+  *out = c;
+  return 0;
+}
+
+int fctn_upload(fctn_ctx* c, const void* x_F, const uint8_t* mask_F) {
+  return fctn::guarded(&c->impl, [&] {
+    Ctx& x = c->impl;
+    const int64_t T = x.sh.total();
+    CK(cudaMemcpyAsync(x.X[0], x_F, T * x.esize, cudaMemcpyHostToDevice, x.st));
+    CK(cudaMemcpyAsync(x.mask, mask_F, T, cudaMemcpyHostToDevice, x.st));
+    CK(cudaStreamSynchronize(x.st));
+    x.cur = 0;
+    x.uploaded = true;
+  });
+}
+
+int fctn_set_factors(fctn_ctx* c, const double* const* a_unf, const int64_t* versions, int reset_cache) {
+  return fctn::guarded(&c->impl, [&] {
+    Ctx& x = c->impl;
+    for (int k = 0; k < x.sh.n; ++k) {
+      int64_t e = x.sh.dims[k] * x.sh.s_of(k);
+      CK(cudaMemcpyAsync(x.A64[k], a_unf[k], e * sizeof(double), cudaMemcpyHostToDevice, x.st));
+      if (x.dtype == FCTN_F32) fctn::launch_convert_f64_f32(x.A64[k], (float*)x.Ac[k], e, x.st);
+      if (versions) x.planner->versions[k] = versions[k];
+    }
+    if (reset_cache) x.planner->reset_cache(&x);
+    CK(cudaStreamSynchronize(x.st));
+  });
+}
+
+int fctn_set_rank(fctn_ctx* c, const int64_t* rank_tri) {
+  return fctn::guarded(&c->impl, [&] {
+    Ctx& x = c->impl;
+    CK(cudaStreamSynchronize(x.st));
+    for (int i = 0; i < x.sh.n * (x.sh.n - 1) / 2; ++i)
+      if (rank_tri[i] < 1) throw fctn::UsageError("rank entries must be >= 1");
+    x.sh.tri.assign(rank_tri, rank_tri + x.sh.n * (x.sh.n - 1) / 2);
+    x.configure_shape();
+  });
+}
+
+int fctn_get_factors(fctn_ctx* c, double* const* a_unf) {
+  return fctn::guarded(&c->impl, [&] {
+    Ctx& x = c->impl;
+    for (int k = 0; k < x.sh.n; ++k) {
+      int64_t e = x.sh.dims[k] * x.sh.s_of(k);
+      CK(cudaMemcpyAsync(a_unf[k], x.A64[k], e * sizeof(double), cudaMemcpyDeviceToHost, x.st));
+    }
+    CK(cudaStreamSynchronize(x.st));
+  });
+}
+
+int fctn_get_x(fctn_ctx* c, void* x_F) {
+  return fctn::guarded(&c->impl, [&] {
+    Ctx& x = c->impl;
+    CK(cudaMemcpyAsync(x_F, x.X[x.cur], x.sh.total() * x.esize, cudaMemcpyDeviceToHost, x.st));
+    CK(cudaStreamSynchronize(x.st));
+  });
+}
+
+int fctn_objective(fctn_ctx* c, double* out, int64_t* counters) {
+  return fctn::guarded(&c->impl, [&] { *out = c->impl.objective(counters); });
+}
+
+int fctn_sweep(fctn_ctx* c, const int32_t* order, int extrap, double alpha, double beta, double* stats,
+               int64_t* counters) {
+  return fctn::guarded(&c->impl, [&] { c->impl.sweep(order, extrap, alpha, beta, stats, counters); });
+}
+
+int fctn_plan_sweeps(int n, const int64_t* dims, const int64_t* rank_tri, int algorithm, int64_t cache_budget,
+                     int n_sweeps, const int32_t* orders, int64_t* counters) {
+  return fctn::guarded(nullptr, [&] {
+    fctn::Shape sh;
+    sh.n = n;
+    sh.dims.assign(dims, dims + n);
+    sh.tri.assign(rank_tri, rank_tri + n * (n - 1) / 2);
+    fctn::Planner pl(sh, cache_budget);
+    pl.versions.assign(n, 0);
+    for (int t = 0; t < n_sweeps; ++t) {
+      std::vector<int> order(orders + (int64_t)t * n, orders + (int64_t)(t + 1) * n);
+      fctn::Meter m0 = pl.meter;
+      int64_t h0 = pl.cache().hits;
+      const int64_t T = sh.total();
+      for (int k : order) {
+        if (algorithm == FCTN_ALG_ACCEL)
+          pl.partial_cached(k, order, nullptr, 0);
+        else
+          pl.partial_plain(k, nullptr, 0);
+        int64_t I = sh.dims[k], S = sh.s_of(k), p = T / I;
+        pl.meter.proj += 2 * I * p * S;
+        pl.meter.gram += 2 * S * S * p;
+        pl.versions[k] += 1;
+      }
+      int kl = order.back();
+      if (algorithm == FCTN_ALG_ACCEL)
+        pl.meter.compose += 2 * (T / sh.dims[kl]) * sh.s_of(kl) * sh.dims[kl];
+      else
+        pl.meter.compose += pl.compose_chain_flops();
+      int64_t* ct = counters + (int64_t)t * FCTN_CT_COUNT;
+      for (int i = 0; i < FCTN_CT_COUNT; ++i) ct[i] = 0;
+      ct[FCTN_CT_FLOPS] = pl.meter.total() - m0.total();
+      ct[FCTN_CT_MK] = pl.meter.mk - m0.mk;
+      ct[FCTN_CT_COMPOSE] = pl.meter.compose - m0.compose;
+      ct[FCTN_CT_HITS] = pl.cache().hits - h0;
+    }
+  });
+}
+
+int fctn_nccl_unique_id(uint8_t* id128) {
+  (void)id128;
+  fctn::g_err = "multi-GPU communicator not built in this library";
+  return 3;
+}
+
+int fctn_set_comm(fctn_ctx* c, const uint8_t* id128, int rank, int nranks, int64_t slab_lo, int64_t slab_hi) {
+  (void)id128;
+  (void)slab_lo;
+  (void)slab_hi;
+  return fctn::guarded(&c->impl, [&] {
+    if (nranks != 1 || rank != 0) throw fctn::UsageError("multi-GPU sharding not available yet");
+  });
+}
+
+int fctn_sync(fctn_ctx* c) {
+  return fctn::guarded(&c->impl, [&] { CK(cudaStreamSynchronize(c->impl.st)); });
+}
+
+const char* fctn_last_error(fctn_ctx* c) { return c ? c->impl.err.c_str() : fctn::g_err.c_str(); }
+
+const char* fctn_version(void) { return "fctn_b200 0.1.0 (sm_100a)"; }
+
+void fctn_destroy(fctn_ctx* c) { delete c; }
+
+}  // extern "C"

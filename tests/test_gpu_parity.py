@@ -1,0 +1,131 @@
+"""GPU parity: the sm_100a sweep through the C ABI against (a) the reference's
+own outputs (golden fixtures) and (b) the CPU oracle at config shapes.
+FP64 tolerance (north_star): <= 1e-9 relative in X and factors."""
+import math
+
+import numpy as np
+import pytest
+
+import paper_2510_22506_b200 as P
+from oracle import fctn_oracle as O
+from paper_2510_22506_b200.workloads import WORKLOADS, make_instance
+from tests.golden_util import load_run, rel, run_case_names
+
+pytestmark = pytest.mark.gpu
+FP64_TOL = 1e-9
+
+
+def _cfg(d):
+    d = dict(d)
+    if d.get("extrapolation") is not None:
+        d["extrapolation"] = tuple(d["extrapolation"])
+    return P.SolverConfig(**d)
+
+
+@pytest.mark.parametrize("name", run_case_names())
+def test_gpu_matches_reference_golden(name):
+    case = load_run(name)
+    res = P.run(P.Observation(case["values"], case["mask"]), _cfg(case["config"]))
+    assert rel(res.x, case["x"]) <= FP64_TOL
+    for k, f in enumerate(case["factors"]):
+        assert res.factors.factor(k).shape == f.shape
+        assert rel(res.factors.factor(k), f) <= FP64_TOL, k
+    assert list(res.factors.versions) == list(case["versions"])
+    assert res.converged == bool(case["converged"])
+    assert res.initial_objective == pytest.approx(float(case["initial_objective"]), rel=1e-11)
+    m = case["mask"]
+    assert np.array_equal(res.x[m], case["values"][m])  # observed entries bit-exact
+    assert len(res.trace) == len(case["trace_objective"])
+    for i, r in enumerate(res.trace):
+        assert r.iteration == i + 1
+        assert r.objective == pytest.approx(case["trace_objective"][i], rel=FP64_TOL)
+        assert r.x_norm == pytest.approx(case["trace_x_norm"][i], rel=1e-10)
+        assert r.factor_norm == pytest.approx(case["trace_factor_norm"][i], rel=FP64_TOL)
+        assert r.step_sq == pytest.approx(case["trace_step_sq"][i], rel=1e-6, abs=1e-12)
+        assert (r.flops, r.mk_flops, r.compose_flops, r.cache_hits) == (
+            case["trace_flops"][i], case["trace_mk_flops"][i], case["trace_compose_flops"][i],
+            case["trace_cache_hits"][i])
+        assert list(r.rank) == list(case["trace_rank"][i])
+        assert r.rank_grown == bool(case["trace_rank_grown"][i])
+
+
+@pytest.mark.parametrize("name,iters", [("c1", 50), ("c2", 50), ("c3", 4)])
+def test_gpu_matches_oracle_fp64_configs(name, iters):
+    wl, truth, mask = make_instance(name)
+    kw = dict(lam=0.35, delta=0.5, rho=0.1, eps=0.0, max_iters=iters, max_rank=wl.rank, initial_rank=wl.rank,
+              rank_policy="fixed", algorithm="afctnlr", shuffle=True, seed=0)
+    ref = O.run(truth, mask, **kw)
+    res = P.run(P.Observation(truth, mask), P.SolverConfig(**kw))
+    assert rel(res.x, ref.x) <= FP64_TOL
+    for k in range(len(wl.dims)):
+        assert rel(res.factors.factor(k), ref.factors[k]) <= FP64_TOL
+    for a, b in zip(res.trace, ref.trace):
+        assert a.objective == pytest.approx(b.objective, rel=FP64_TOL)
+        assert (a.flops, a.mk_flops, a.compose_flops, a.cache_hits) == (b.flops, b.mk_flops, b.compose_flops,
+                                                                         b.cache_hits)
+    assert abs(O.psnr(res.x, truth) - O.psnr(ref.x, truth)) <= 1e-6
+
+
+@pytest.mark.parametrize("name,dims,iters", [("c4", (256, 256, 64), 20), ("c5", (20, 20, 20, 20, 20), 20)])
+def test_gpu_fp32_variant_scaled(name, dims, iters):
+    """FP32 variant against the FP64 oracle on the same (fp32-rounded) data:
+    bound 5e-3 relative in X, |dPSNR| <= 0.01 dB (north_star)."""
+    wl, truth, mask = make_instance(name, dims=dims)
+    kw = dict(lam=0.35, delta=0.5, rho=0.1, eps=0.0, max_iters=iters, max_rank=wl.rank, initial_rank=wl.rank,
+              rank_policy="fixed", algorithm="afctnlr", shuffle=True, seed=0)
+    ref = O.run(truth, mask, **kw)
+    res = P.run(P.Observation(truth, mask), P.SolverConfig(**kw), dtype="float32")
+    peak = float(np.max(np.abs(truth)))
+    dpsnr = abs(O.psnr(res.x, truth, peak) - O.psnr(ref.x, truth, peak))
+    assert rel(res.x, ref.x) <= 5e-3
+    assert dpsnr <= 0.01
+    m = mask
+    assert np.array_equal(res.x[m], truth.astype(np.float32).astype(np.float64)[m])
+
+
+def test_gpu_run_is_deterministic():
+    case = load_run("n4_afctnlr_shuffle")
+    a = P.run(P.Observation(case["values"], case["mask"]), _cfg(case["config"]))
+    b = P.run(P.Observation(case["values"], case["mask"]), _cfg(case["config"]))
+    assert np.array_equal(a.x, b.x)
+    for k in range(a.factors.n):
+        assert np.array_equal(a.factors.factor(k), b.factors.factor(k))
+    assert [r.objective for r in a.trace] == [r.objective for r in b.trace]
+
+
+def test_gpu_as_printed_orientation_raises():
+    case = load_run("n3_afctnlr")
+    cfg = _cfg(dict(case["config"], laplacian_sign="as-printed", lam=1.0))
+    with pytest.raises(P.NumericalFailure):
+        P.run(P.Observation(case["values"], case["mask"]), cfg)
+
+
+def test_gpu_validation_errors():
+    case = load_run("n3_afctnlr")
+    obs = P.Observation(case["values"], case["mask"])
+    with pytest.raises(ValueError):
+        P.run(obs, P.SolverConfig(initial_rank=3, max_rank=2))
+    with pytest.raises(ValueError):
+        P.run(obs, P.SolverConfig(lam=-0.5))
+    with pytest.raises(ValueError):
+        P.run(obs, P.SolverConfig(lam=(0.1, 0.2)))
+    with pytest.raises(ValueError):
+        P.run(obs, P.SolverConfig(delta=0.0))
+
+
+def test_gpu_sufficient_decrease():
+    """f_{t+1} + rho/2 step^2 <= f_t (test_solver.py:283-294)."""
+    case = load_run("n3_afctnlr")
+    rng = np.random.default_rng(17)
+    dims = (7, 6, 5)
+    truth = rng.standard_normal(dims)
+    from paper_2510_22506_b200.workloads import sample_mask
+    obs = P.Observation(truth, sample_mask(dims, 0.35, 17))
+    cfg = P.SolverConfig(lam=0.35, delta=0.5, rho=0.1, eps=0.0, max_iters=60, max_rank=2, rank_policy="fixed",
+                         initial_rank=2, seed=0, algorithm="afctnlr")
+    res = P.run(obs, cfg)
+    prev = res.initial_objective
+    for rec in res.trace:
+        assert rec.objective + 0.5 * cfg.rho * rec.step_sq <= prev + 1e-9 * abs(prev)
+        prev = rec.objective
+    assert case is not None
