@@ -323,9 +323,11 @@ class Ctx : public Executor {
     A64.assign(n, nullptr);
     Ac.assign(n, nullptr);
     for (int k = 0; k < n; ++k) {
+      // every fp64 factor slot has the max size: the solve output buffer is
+      // swapped with the factor it replaces, so slots migrate between modes
       int64_t e = sh.dims[k] * sh.s_of(k);
-      CK(cudaMalloc(&A64[k], e * sizeof(double)));
-      CK(cudaMemset(A64[k], 0, e * sizeof(double)));
+      CK(cudaMalloc(&A64[k], max_is * sizeof(double)));
+      CK(cudaMemset(A64[k], 0, max_is * sizeof(double)));
       if (dtype == FCTN_F32) {
         CK(cudaMalloc(&Ac[k], e * sizeof(float)));
       } else {
