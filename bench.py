@@ -1,0 +1,327 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 PAM sweep (BASELINE.json metric: PAM iterations/sec
+per full sweep and achieved HBM GB/s vs roofline).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c4] [--impl ours|reference]
+
+One step = one PAM sweep (solver.py:307-395) over the whole synthetic tensor
+of the chosen config (default c4: 2048x2048x64 fp32, R=8, SR=0.1 — the
+largest config, the one the metric is quoted on at 1/2/4/8 GPUs).  `value`
+is device-timed (CUDA events on the library's stream) with X, mask, factors
+and the reuse cache resident in HBM; `e2e` is the same metric through the
+public `run(obs, cfg)` call from host arrays (upload, K sweeps, download).
+`--impl reference` times the CPU oracle port of the reference algorithm on
+the host cores (rank 0 only).  Prints one JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_2510_22506_b200.workloads import WORKLOADS, make_instance  # noqa: E402
+
+METRIC = "PAM iterations/sec (full sweep)"
+UNIT = "iter/s"
+PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "source": "fallback (B200_PROFILING.md)"}
+SOLVER_KW = dict(lam=0.35, delta=0.5, rho=0.1, eps=0.0, rank_policy="fixed", algorithm="afctnlr", shuffle=True,
+                 seed=0)
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return {"hbm_gbs": float(d["hbm_gbs"]), "source": "measured (MEASURED_PEAKS.json)"}
+    return dict(PEAKS_FALLBACK)
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        try:
+            fd, self.path = tempfile.mkstemp(suffix=".csv")
+            os.close(fd)
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+            time.sleep(0.25)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        time.sleep(0.15)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        rows = []
+        for line in open(self.path):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 6:
+                rows.append(parts)
+        os.unlink(self.path)
+        if not rows:
+            return None
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        loaded = [v for v in sm if v > 500] or sm
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[2 + i].lower().startswith("active")})
+        return {"sm_mhz": float(np.median(loaded)) if loaded else None,
+                "sm_max_mhz": float(rows[0][1]) if rows[0][1].replace(".", "").isdigit() else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+def m_sizes(dims, rank):
+    n = len(dims)
+    T = math.prod(dims)
+    return [rank ** (n - 1) * (T // dims[k]) for k in range(n)]
+
+
+def sweep_bytes(dims, rank, b, last_modes):
+    """B_stream = b(N T + sum_k |M_k| + |M_last| + 2T) + T/8 and
+    B_min = b(N+2)T + T/8, per sweep (mean over the visited orders)."""
+    n = len(dims)
+    T = math.prod(dims)
+    ms = m_sizes(dims, rank)
+    bs = [b * (n * T + sum(ms) + ms[k] + 2 * T) + T / 8 for k in last_modes]
+    return float(np.mean(bs)), float(b * (n + 2) * T + T / 8)
+
+
+def cpu_sample(name, wl, truth, mask, max_seconds=20.0, warm=1, steps=None):
+    """Oracle (CPU port of the reference algorithm) per-sweep time on the host
+    cores.  c4/c5 use a mode-0 slab (1/16 of the tensor; the sweep cost is
+    linear in T at fixed ranks) and scale the time up."""
+    from oracle import fctn_oracle as O
+
+    frac = 1
+    if wl.total > 20_000_000:
+        frac = 16
+        rows = max(wl.dims[0] // frac, 1)
+        frac = wl.dims[0] / rows
+        truth = np.asfortranarray(truth[:rows])
+        mask = np.asfortranarray(mask[:rows])
+    walls = []
+    t_start = time.perf_counter()
+
+    def on_iter(rec):
+        walls.append(rec.wall_ms)
+        if steps is None and time.perf_counter() - t_start > max_seconds and len(walls) > warm:
+            raise StopIteration
+
+    iters = (warm + steps) if steps is not None else 10_000
+    try:
+        O.run(truth, mask, max_iters=iters, max_rank=wl.rank, initial_rank=wl.rank, on_iter=on_iter, **SOLVER_KW)
+    except StopIteration:
+        pass
+    timed = walls[warm:] if len(walls) > warm else walls
+    ms = float(np.sum(timed)) * frac
+    cores = len(os.sched_getaffinity(0))
+    sample = (f"{'mode-0 slab ' + 'x'.join(map(str, truth.shape)) + f' (1/{frac:g} of {name}), time x{frac:g}' if frac > 1 else 'full ' + name}; "
+              f"{len(timed)} sweeps after {warm} warm-up; numpy BLAS threads={cores}")
+    return {"value": len(timed) / (ms / 1e3), "unit": UNIT, "cores": cores, "kind": "port", "sample": sample,
+            "ms_per_sweep": ms / len(timed)}, len(timed), ms
+
+
+def run_reference(args, wl, name):
+    ws, rank, local = dist_env()
+    if rank != 0:
+        return 0
+    wl_, truth, mask = make_instance(name)
+    cb, k_done, ms = cpu_sample(name, wl, truth, mask, warm=args.warmup, steps=args.steps)
+    cb["value"] = round(cb["value"], 6)
+    line = {"metric": METRIC, "value": cb["value"], "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms / k_done, 3),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": config_of(name, wl, 1),
+            "cpu_baseline": cb, "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
+                                        "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+    return 0
+
+
+def config_of(name, wl, nranks):
+    return {"workload": f"{name}: {wl.note}", "dims": list(wl.dims), "rank": wl.rank, "sample_rate": wl.sample_rate,
+            "solver": "afctnlr, lam=0.35 delta=0.5 rho=0.1, fixed rank, shuffled orders, seed 0",
+            "parallelism": f"replicas x{nranks}" if nranks > 1 else "single GPU",
+            "l2": "inputs larger than the 126 MB L2; no flush" if wl.total * 4 > 126e6 else
+                  "working set L2-resident (latency-bound config)"}
+
+
+def load_traffic(name):
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if not os.path.exists(p):
+        return {}
+    try:
+        return json.load(open(p)).get(name, {})
+    except Exception:
+        return {}
+
+
+def run_ours(args, wl, name):
+    import paper_2510_22506_b200 as P
+    from paper_2510_22506_b200 import _native
+    from paper_2510_22506_b200.network import FctnFactors, FctnRank
+
+    ws, rank, local = dist_env()
+    dist = None
+    if ws > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    wl, truth, mask = make_instance(name)
+    n = len(wl.dims)
+    dt = _native.F32 if wl.dtype == "f32" else _native.F64
+    b = 4 if dt == _native.F32 else 8
+    rk = FctnRank.uniform(n, wl.rank)
+    obs = P.Observation(truth, mask)
+    ctx = _native.Context(local, dt, wl.dims, rk.entries, (0.35,) * n, (0.5,) * n, _native.SIGN_PD, 0.1,
+                          _native.ALG_ACCEL, 1 << 30, numeric_exc=P.NumericalFailure)
+    ctx.upload(obs.values, obs.mask)
+    rng = np.random.default_rng(0)
+    f = FctnFactors.random(wl.dims, rk, rng)
+    ctx.set_factors(f.unfoldings(), f.versions, True)
+    ctx.objective()
+    order = tuple(range(n))
+    for _ in range(args.warmup):
+        ctx.sweep(order)
+        order = tuple(int(v) for v in rng.permutation(n))
+    ctx.set_profiling(True)
+    clocks = Clocks(local)
+    if dist is not None:
+        dist.barrier()
+    ctx.sync()
+    clocks.start()
+    ctx.timer_start()
+    launches = 0
+    lasts = []
+    flops = 0
+    for _ in range(args.steps):
+        stats, ct = ctx.sweep(order)
+        launches += int(ct[_native.CT_LAUNCHES])
+        flops += int(ct[_native.CT_FLOPS])
+        lasts.append(order[-1])
+        order = tuple(int(v) for v in rng.permutation(n))
+    ms = ctx.timer_stop()
+    clk = clocks.stop()
+    prof = ctx.get_profile()
+    ctx.set_profiling(False)
+    if dist is not None:
+        import torch
+
+        t = torch.tensor([ms], device=f"cuda:{local}", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ctx.close()
+    ms_step = ms / args.steps
+    value = ws * args.steps / (ms / 1e3)
+
+    # ---- roofline of the dominant kernel class (largest share of the timed region)
+    pk = peaks()
+    dom = max(prof.items(), key=lambda kv: kv[1]["ms"])
+    dname, d = dom
+    per_launch_ms = d["ms"] / max(d["launches"], 1)
+    per_launch_bytes = d["bytes"] / max(d["launches"], 1)
+    achieved = per_launch_bytes / (per_launch_ms / 1e3) / 1e9
+    traffic = load_traffic(name).get(dname)
+    roofline = {"bound": "hbm", "kernel": dname, "achieved": round(achieved, 1), "peak": pk["hbm_gbs"],
+                "unit": "GB/s", "frac": round(achieved / pk["hbm_gbs"], 4), "traffic": traffic,
+                "peak_source": pk["source"], "share_of_step": round(d["ms"] / ms, 4),
+                "launch_ms": round(per_launch_ms, 4), "algorithmic_bytes_per_launch": per_launch_bytes}
+    bst, bmin = sweep_bytes(wl.dims, wl.rank, b, lasts)
+    sweep_roof = {"B_stream_GB": round(bst / 1e9, 4), "B_min_GB": round(bmin / 1e9, 4),
+                  "achieved_GBs": round(bst / (ms_step / 1e3) / 1e9, 1),
+                  "frac": round(bst / (ms_step / 1e3) / 1e9 / pk["hbm_gbs"], 4),
+                  "flops_ref_per_sweep": flops // args.steps}
+    kernels = {k: {"ms_per_step": round(v["ms"] / args.steps, 4), "launches_per_step": v["launches"] / args.steps,
+                   "GBs": round(v["bytes"] / (v["ms"] / 1e3) / 1e9, 1) if v["ms"] > 0 else None}
+               for k, v in prof.items()}
+
+    # ---- e2e through the public API from host arrays
+    cfg = P.SolverConfig(max_iters=args.steps, max_rank=wl.rank, initial_rank=wl.rank, **SOLVER_KW)
+    if dist is not None:
+        dist.barrier()
+    t0 = time.perf_counter()
+    res = P.run(obs, cfg, dtype="float32" if dt == _native.F32 else "float64", device=local)
+    t_e2e = time.perf_counter() - t0
+    if dist is not None:
+        import torch
+
+        t = torch.tensor([t_e2e], device=f"cuda:{local}", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t_e2e = float(t.item())
+    T = wl.total
+    fac_bytes = sum(8 * wl.dims[k] * wl.rank ** (n - 1) for k in range(n))
+    e2e = {"value": round(ws * len(res.trace) / t_e2e, 4), "unit": UNIT,
+           "h2d_bytes_per_step": int((T * b + T + fac_bytes) / len(res.trace)),
+           "d2h_bytes_per_step": int((T * b + fac_bytes) / len(res.trace)),
+           "note": "one run(obs, cfg) call: setup + upload + K sweeps + download, bytes amortised per sweep"}
+    del res
+
+    cpu = None
+    if ws == 1 and not args.no_cpu_baseline:
+        cpu, _, _ = cpu_sample(name, wl, truth, mask)
+        cpu["value"] = round(cpu["value"], 6)
+    if rank == 0:
+        line = {"metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": round(ms_step, 4), "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": wl.dtype, "data": "synthetic",
+                "config": config_of(name, wl, ws), "roofline": roofline, "sweep_roofline": sweep_roof,
+                "kernels": kernels, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk}
+        print(json.dumps(line))
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c4", choices=sorted(WORKLOADS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        args.warmup = 3
+    wl = WORKLOADS[args.config]
+    if args.impl == "reference":
+        return run_reference(args, wl, args.config)
+    return run_ours(args, wl, args.config)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -123,8 +123,26 @@ int fctn_nccl_unique_id(uint8_t* id128);
 int fctn_set_comm(fctn_ctx* ctx, const uint8_t* id128, int rank, int nranks, int64_t slab_lo,
                   int64_t slab_hi);
 
-/* Sync the context stream and return the device time of the last sweep. */
+/* Sync the context stream. */
 int fctn_sync(fctn_ctx* ctx);
+
+/* Device timer on the context stream: op 0 records the start event, op 1
+ * records the stop event, synchronises and writes the elapsed ms. */
+int fctn_timer(fctn_ctx* ctx, int op, double* ms);
+
+/* Per-kernel-class profiling with CUDA events on the launching stream.
+ * Classes: FCTN_K_* below.  When on, every launch group is bracketed by
+ * events; fctn_get_profile returns accumulated ms, launch counts and the
+ * algorithmic bytes per class since the last reset. */
+#define FCTN_K_MERGE 0    /* K1 contraction (partials, M_k) */
+#define FCTN_K_STREAM_Y 1 /* K2 X_(k) M_k^T */
+#define FCTN_K_GRAM 2     /* K2 M_k M_k^T */
+#define FCTN_K_REDUCE 3   /* split-K reductions */
+#define FCTN_K_SOLVE 4    /* K3 DFT / Cholesky / inverse / stats */
+#define FCTN_K_COMPOSE 5  /* K4 compose + blend + reductions */
+#define FCTN_K_COUNT 8
+int fctn_set_profiling(fctn_ctx* ctx, int on);
+int fctn_get_profile(fctn_ctx* ctx, double* ms, int64_t* launches, double* bytes);
 
 const char* fctn_last_error(fctn_ctx* ctx);
 const char* fctn_version(void);

@@ -24,8 +24,10 @@ CT_FLOPS, CT_MK, CT_COMPOSE, CT_HITS, CT_LAUNCHES, CT_COUNT = 0, 1, 2, 3, 4, 8
 EXPORTS = [
     "fctn_create", "fctn_upload", "fctn_set_factors", "fctn_set_rank", "fctn_get_factors", "fctn_get_x",
     "fctn_objective", "fctn_sweep", "fctn_plan_sweeps", "fctn_nccl_unique_id", "fctn_set_comm",
-    "fctn_sync", "fctn_last_error", "fctn_version", "fctn_destroy",
+    "fctn_sync", "fctn_timer", "fctn_set_profiling", "fctn_get_profile", "fctn_last_error", "fctn_version",
+    "fctn_destroy",
 ]
+K_CLASSES = ["merge", "stream_y", "gram", "reduce", "solve", "compose", "k6", "k7"]
 
 _lib = None
 
@@ -59,6 +61,9 @@ def lib():
     L.fctn_nccl_unique_id.argtypes = [P]
     L.fctn_set_comm.argtypes = [P, P, C.c_int, C.c_int, C.c_int64, C.c_int64]
     L.fctn_sync.argtypes = [P]
+    L.fctn_timer.argtypes = [P, C.c_int, f64p]
+    L.fctn_set_profiling.argtypes = [P, C.c_int]
+    L.fctn_get_profile.argtypes = [P, f64p, i64p, f64p]
     L.fctn_last_error.argtypes = [P]
     L.fctn_last_error.restype = C.c_char_p
     L.fctn_version.argtypes = []
@@ -193,3 +198,24 @@ class Context:
 
     def sync(self):
         self._check(lib().fctn_sync(self.h))
+
+    def timer_start(self):
+        self._check(lib().fctn_timer(self.h, 0, None))
+
+    def timer_stop(self) -> float:
+        v = C.c_double()
+        self._check(lib().fctn_timer(self.h, 1, C.byref(v)))
+        return float(v.value)
+
+    def set_profiling(self, on: bool):
+        self._check(lib().fctn_set_profiling(self.h, int(bool(on))))
+
+    def get_profile(self) -> dict:
+        ms = np.zeros(8)
+        n = np.zeros(8, dtype=np.int64)
+        b = np.zeros(8)
+        self._check(lib().fctn_get_profile(self.h, ms.ctypes.data_as(C.POINTER(C.c_double)),
+                                           n.ctypes.data_as(C.POINTER(C.c_int64)),
+                                           b.ctypes.data_as(C.POINTER(C.c_double))))
+        return {K_CLASSES[i]: {"ms": float(ms[i]), "launches": int(n[i]), "bytes": float(b[i])}
+                for i in range(8) if n[i] > 0}

@@ -87,6 +87,58 @@ class Ctx : public Executor {
   bool configured = false;
   bool uploaded = false;
 
+  // profiling: events bracketing launch groups, accumulated per class
+  struct Mark {
+    int cls;
+    cudaEvent_t a, b;
+    double bytes;
+    int64_t n;
+  };
+  bool prof = false;
+  std::vector<Mark> marks;
+  std::vector<cudaEvent_t> evpool;
+  double prof_ms[FCTN_K_COUNT] = {0};
+  int64_t prof_n[FCTN_K_COUNT] = {0};
+  double prof_bytes[FCTN_K_COUNT] = {0};
+  cudaEvent_t tstart = nullptr, tstop = nullptr;
+
+  cudaEvent_t take_event() {
+    if (!evpool.empty()) {
+      cudaEvent_t e = evpool.back();
+      evpool.pop_back();
+      return e;
+    }
+    cudaEvent_t e;
+    CK(cudaEventCreate(&e));
+    return e;
+  }
+  int pbegin(int cls) {
+    if (!prof) return -1;
+    Mark m{cls, take_event(), take_event(), 0.0, 0};
+    CK(cudaEventRecord(m.a, st));
+    marks.push_back(m);
+    return (int)marks.size() - 1;
+  }
+  void pend(int idx, double bytes, int64_t n) {
+    if (idx < 0) return;
+    Mark& m = marks[idx];
+    m.bytes = bytes;
+    m.n = n;
+    CK(cudaEventRecord(m.b, st));
+  }
+  void collect_marks() {  // after a stream sync
+    for (auto& m : marks) {
+      float ms = 0.f;
+      CK(cudaEventElapsedTime(&ms, m.a, m.b));
+      prof_ms[m.cls] += ms;
+      prof_n[m.cls] += m.n;
+      prof_bytes[m.cls] += m.bytes;
+      evpool.push_back(m.a);
+      evpool.push_back(m.b);
+    }
+    marks.clear();
+  }
+
   ~Ctx() override { release_all(); }
 
   // ------------------------------------------------------------ executor
@@ -223,6 +275,7 @@ class Ctx : public Executor {
 
   void contract(const ContractOp& op) override {
     Tables& t = tables_for(op);
+    int pm = pbegin(FCTN_K_MERGE);
     const void* ra = ptr_of(t.swap ? op.b : op.a);
     const void* cb = ptr_of(t.swap ? op.a : op.b);
     void* out = ptr_of(op.out);
@@ -236,6 +289,7 @@ class Ctx : public Executor {
       launch_contract<float>((const float*)ra, (const float*)cb, (float*)out, rowA, rowC, colB, colC, kA, kB,
                              t.rows, t.cols, t.K, st);
     ++launches;
+    pend(pm, (double)esize * (op.out.numel(sh) + op.a.numel(sh) + op.b.numel(sh)), 1);
   }
 
   void permute(const LTensor& in, const LTensor& out) override {
@@ -433,15 +487,23 @@ class Ctx : public Executor {
     for (int j = 0; j < k; ++j) P *= sh.dims[j];
     StreamPlan sy = plan_stream(I, S, p, target_ctas());
     StreamPlan sg = plan_stream(S, S, p, target_ctas());
-    if (dtype == FCTN_F64) {
+    int pm = pbegin(FCTN_K_STREAM_Y);
+    if (dtype == FCTN_F64)
       launch_stream<double>((const double*)X[cur], (const double*)Mbuf, ypart, I, P, S, p, sy, st);
-      launch_stream<double>((const double*)Mbuf, (const double*)Mbuf, gpart, S, 1, S, p, sg, st);
-    } else {
+    else
       launch_stream<float>((const float*)X[cur], (const float*)Mbuf, ypart, I, P, S, p, sy, st);
+    pend(pm, (double)esize * (T + S * p), 1);
+    pm = pbegin(FCTN_K_GRAM);
+    if (dtype == FCTN_F64)
+      launch_stream<double>((const double*)Mbuf, (const double*)Mbuf, gpart, S, 1, S, p, sg, st);
+    else
       launch_stream<float>((const float*)Mbuf, (const float*)Mbuf, gpart, S, 1, S, p, sg, st);
-    }
+    pend(pm, (double)esize * S * p, 1);
+    pm = pbegin(FCTN_K_REDUCE);
     launch_reduce_y(ypart, sy.nsplit, I, S, A64[k], rho, Y, st);
     launch_reduce_g(gpart, sg.nsplit, S, G, st);
+    pend(pm, 8.0 * ((double)sy.nsplit * I * S + (double)sg.nsplit * S * S), 2);
+    pm = pbegin(FCTN_K_SOLVE);
     planner->meter.proj += 2 * I * p * S;   // sylvester.py:105
     planner->meter.gram += 2 * S * S * p;   // sylvester.py:58
     const int64_t H1 = I / 2 + 1;
@@ -454,6 +516,7 @@ class Ctx : public Executor {
                             st);
     const double sgn = sign == FCTN_SIGN_PD ? -1.0 : 1.0;
     launch_factor_stats(Ascratch, A64[k], I, S, delta[k], sgn, dstats + 3 * k, st);
+    pend(pm, 8.0 * (4.0 * I * S + S * S), 4);
     std::swap(A64[k], Ascratch);
     if (dtype == FCTN_F64) Ac[k] = A64[k];
     launches += 9;
@@ -466,6 +529,7 @@ class Ctx : public Executor {
     int64_t P = 1;
     for (int j = 0; j < k; ++j) P *= sh.dims[j];
     int nb;
+    int pm = pbegin(FCTN_K_COMPOSE);
     if (dtype == FCTN_F64)
       nb = launch_compose<double>((const double*)Ac[k], (const double*)Mbuf, (const double*)X[cur], mask,
                                   (double*)X[cur ^ 1], I, P, S, p, rho, objective_only, partials, partial_cap, st);
@@ -474,6 +538,7 @@ class Ctx : public Executor {
                                  (float*)X[cur ^ 1], I, P, S, p, rho, objective_only, partials, partial_cap, st);
     launch_reduce4(partials, nb, dstats + 3 * sh.n, st);
     launches += 2;
+    pend(pm, objective_only ? (double)esize * (S * p + T) : (double)esize * (S * p + 2 * T) + (double)T, 2);
   }
 
   void fetch_stats() {
@@ -481,6 +546,7 @@ class Ctx : public Executor {
     CK(cudaMemcpyAsync(hstats, dstats, (n * 3 + 4) * sizeof(double), cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync((char*)(hstats + n * 3 + 8), dstatus, sizeof(int), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
+    collect_marks();
     int status;
     std::memcpy(&status, (char*)(hstats + n * 3 + 8), sizeof(int));
     if (status) {
@@ -744,6 +810,48 @@ int fctn_set_comm(fctn_ctx* c, const uint8_t* id128, int rank, int nranks, int64
   (void)slab_hi;
   return fctn::guarded(&c->impl, [&] {
     if (nranks != 1 || rank != 0) throw fctn::UsageError("multi-GPU sharding not available yet");
+  });
+}
+
+int fctn_timer(fctn_ctx* c, int op, double* ms) {
+  return fctn::guarded(&c->impl, [&] {
+    Ctx& x = c->impl;
+    if (!x.tstart) {
+      CK(cudaEventCreate(&x.tstart));
+      CK(cudaEventCreate(&x.tstop));
+    }
+    if (op == 0) {
+      CK(cudaEventRecord(x.tstart, x.st));
+    } else {
+      CK(cudaEventRecord(x.tstop, x.st));
+      CK(cudaEventSynchronize(x.tstop));
+      float f = 0.f;
+      CK(cudaEventElapsedTime(&f, x.tstart, x.tstop));
+      if (ms) *ms = f;
+    }
+  });
+}
+
+int fctn_set_profiling(fctn_ctx* c, int on) {
+  return fctn::guarded(&c->impl, [&] {
+    Ctx& x = c->impl;
+    x.prof = on != 0;
+    for (int i = 0; i < FCTN_K_COUNT; ++i) {
+      x.prof_ms[i] = 0;
+      x.prof_n[i] = 0;
+      x.prof_bytes[i] = 0;
+    }
+  });
+}
+
+int fctn_get_profile(fctn_ctx* c, double* ms, int64_t* launches, double* bytes) {
+  return fctn::guarded(&c->impl, [&] {
+    Ctx& x = c->impl;
+    for (int i = 0; i < FCTN_K_COUNT; ++i) {
+      ms[i] = x.prof_ms[i];
+      launches[i] = x.prof_n[i];
+      bytes[i] = x.prof_bytes[i];
+    }
   });
 }
 
