@@ -269,6 +269,10 @@ def run_ours(args, wl, name):
                for k, v in prof.items()}
 
     # ---- e2e through the public API from host arrays
+    e2e = None
+    if args.no_e2e:
+        return emit_line(args, ws, rank, value, ms_step, wl, name, roofline, sweep_roof, kernels, None, launches, clk,
+                         dist)
     cfg = P.SolverConfig(max_iters=args.steps, max_rank=wl.rank, initial_rank=wl.rank, **SOLVER_KW)
     if dist is not None:
         dist.barrier()
@@ -293,6 +297,12 @@ def run_ours(args, wl, name):
     if ws == 1 and not args.no_cpu_baseline:
         cpu, _, _ = cpu_sample(name, wl, truth, mask)
         cpu["value"] = round(cpu["value"], 6)
+    return emit_line(args, ws, rank, value, ms_step, wl, name, roofline, sweep_roof, kernels, e2e, launches, clk,
+                     dist, cpu)
+
+
+def emit_line(args, ws, rank, value, ms_step, wl, name, roofline, sweep_roof, kernels, e2e, launches, clk, dist,
+              cpu=None):
     if rank == 0:
         line = {"metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": ws, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": round(ms_step, 4), "higher_is_better": True,
@@ -314,6 +324,7 @@ def main():
     ap.add_argument("--config", default="c4", choices=sorted(WORKLOADS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true", help="skip the run(obs, cfg) leg (profiling runs)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3
