@@ -75,9 +75,13 @@ class Ctx : public Executor {
   double* Ascratch = nullptr;
   void* Mbuf = nullptr;
   double *Y = nullptr, *G = nullptr, *Fr = nullptr, *Fi = nullptr;
-  double *ypart = nullptr, *gpart = nullptr;
+  double* ypart = nullptr;
   double* partials = nullptr;
   int64_t partial_cap = 0;
+  std::vector<double*> E64;               // E_j = A_(j)^T A_(j), the doubled-network nodes
+  double *epart = nullptr, *colstats = nullptr;
+  double* gnet[2] = {nullptr, nullptr};   // doubled-network intermediates
+  std::vector<DftPlan> dft;
   std::vector<double*> mu, cosT, sinT;
   std::vector<double> check_mu;
   double* dstats = nullptr;  // [n*3 factor stats][4 sums]
@@ -322,10 +326,13 @@ class Ctx : public Executor {
     }
     A64.clear();
     Ac.clear();
-    for (auto* p : {Ascratch, (double*)Mbuf, Y, G, Fr, Fi, ypart, gpart, partials}) cudaFree(p);
+    for (auto* p : {Ascratch, (double*)Mbuf, Y, G, Fr, Fi, ypart, partials, epart, colstats, gnet[0], gnet[1]})
+      cudaFree(p);
+    for (auto* p : E64) cudaFree(p);
+    E64.clear();
     Ascratch = nullptr;
     Mbuf = nullptr;
-    Y = G = Fr = Fi = ypart = gpart = partials = nullptr;
+    Y = G = Fr = Fi = ypart = partials = epart = colstats = gnet[0] = gnet[1] = nullptr;
   }
   void release_all() {
     if (st) cudaStreamSynchronize(st);
@@ -361,27 +368,29 @@ class Ctx : public Executor {
     release_shape_buffers();
     const int n = sh.n;
     const int64_t T = sh.total();
-    int64_t max_is = 1, max_ss = 1, max_m = 1, max_h = 1, max_yp = 1, max_gp = 1, max_part = 1;
+    int64_t max_is = 1, max_ss = 1, max_m = 1, max_h = 1, max_yp = 1, max_part = 1, max_ep = 1, max_s = 1;
     for (int k = 0; k < n; ++k) {
       int64_t I = sh.dims[k], S = sh.s_of(k), p = T / I;
       max_is = std::max(max_is, I * S);
       max_ss = std::max(max_ss, S * S);
+      max_s = std::max(max_s, S);
       max_m = std::max(max_m, S * p);
       max_h = std::max(max_h, (I / 2 + 1) * S);
       StreamPlan sy = plan_stream(I, S, p, target_ctas());
-      StreamPlan sg = plan_stream(S, S, p, target_ctas());
       max_yp = std::max(max_yp, (int64_t)sy.nsplit * I * S);
-      max_gp = std::max(max_gp, (int64_t)sg.nsplit * S * S);
       max_part = std::max(max_part, ((I + 63) / 64) * ((p + 63) / 64));
+      max_ep = std::max(max_ep, (int64_t)fgram_splits(I) * S * S);
     }
     A64.assign(n, nullptr);
     Ac.assign(n, nullptr);
+    E64.assign(n, nullptr);
     for (int k = 0; k < n; ++k) {
       // every fp64 factor slot has the max size: the solve output buffer is
       // swapped with the factor it replaces, so slots migrate between modes
       int64_t e = sh.dims[k] * sh.s_of(k);
       CK(cudaMalloc(&A64[k], max_is * sizeof(double)));
       CK(cudaMemset(A64[k], 0, max_is * sizeof(double)));
+      CK(cudaMalloc(&E64[k], max_ss * sizeof(double)));
       if (dtype == FCTN_F32) {
         CK(cudaMalloc(&Ac[k], e * sizeof(float)));
       } else {
@@ -395,12 +404,97 @@ class Ctx : public Executor {
     CK(cudaMalloc(&Fr, max_h * sizeof(double)));
     CK(cudaMalloc(&Fi, max_h * sizeof(double)));
     CK(cudaMalloc(&ypart, max_yp * sizeof(double)));
-    CK(cudaMalloc(&gpart, max_gp * sizeof(double)));
+    CK(cudaMalloc(&epart, max_ep * sizeof(double)));
+    CK(cudaMalloc(&colstats, max_s * 3 * sizeof(double)));
     partial_cap = max_part;
     CK(cudaMalloc(&partials, max_part * 4 * sizeof(double)));
+    int64_t gcap = max_ss;
+    for (int k = 0; k < n; ++k) gcap = std::max(gcap, gram_network_peak(k));
+    CK(cudaMalloc(&gnet[0], gcap * sizeof(double)));
+    CK(cudaMalloc(&gnet[1], gcap * sizeof(double)));
     std::vector<int64_t> versions = planner ? planner->versions : std::vector<int64_t>(n, 0);
     planner.reset(new Planner(sh, budget));
     planner->versions = versions;
+  }
+
+  // ------------------------------------------------------------ Gram of M_k
+  // G_k = M_k M_k^T without forming it from M_k: the doubled network of the
+  // factor Grams E_j = A_(j)^T A_(j) (j != k) contracted over every internal
+  // bond and its primed twin.  Same value as sylvester.py:57-59, ~1e-16 apart;
+  // cost ~ s^2 R^2 instead of 2 s^2 p_k (hard part 8).
+  int64_t numel_of(const std::vector<int>& labels) const {
+    int64_t e = 1;
+    for (int l : labels) e *= sh.extent(l);
+    return e;
+  }
+  static std::vector<int> contract_out_labels(const std::vector<int>& a, const std::vector<int>& b) {
+    std::vector<int> out;
+    for (int l : a)
+      if (std::find(b.begin(), b.end(), l) == b.end()) out.push_back(l);
+    for (int l : b)
+      if (std::find(a.begin(), a.end(), l) == a.end()) out.push_back(l);
+    return out;
+  }
+  int64_t gram_network_peak(int k) const {
+    int64_t peak = 1;
+    std::vector<int> cur;
+    bool first = true;
+    for (int j = 0; j < sh.n; ++j) {
+      if (j == k) continue;
+      if (first) {
+        cur = sh.e_labels(j);
+        first = false;
+        continue;
+      }
+      cur = contract_out_labels(cur, sh.e_labels(j));
+      peak = std::max(peak, numel_of(cur));
+    }
+    return peak;
+  }
+  void gram_network(int k) {
+    std::vector<int> rest;
+    for (int j = 0; j < sh.n; ++j)
+      if (j != k) rest.push_back(j);
+    const int64_t S = sh.s_of(k);
+    if (rest.size() == 1) {  // n == 2: G_k = E_j
+      CK(cudaMemcpyAsync(G, E64[rest[0]], S * S * sizeof(double), cudaMemcpyDeviceToDevice, st));
+      return;
+    }
+    LTensor cur;
+    cur.labels = sh.e_labels(rest[0]);
+    const double* cur_ptr = E64[rest[0]];
+    int ping = 0;
+    for (size_t q = 1; q < rest.size(); ++q) {
+      ContractOp op;
+      op.a = cur;
+      op.b.labels = sh.e_labels(rest[q]);
+      const bool last = q + 1 == rest.size();
+      op.out.labels = last ? sh.g_labels(k) : contract_out_labels(op.a.labels, op.b.labels);
+      double* out_ptr = last ? G : gnet[ping];
+      Tables& t = tables_for(op);
+      const double* pa = cur_ptr;
+      const double* pb = E64[rest[q]];
+      const double* ra = t.swap ? pb : pa;
+      const double* cb = t.swap ? pa : pb;
+      const int64_t* d = t.d;
+      launch_contract<double>(ra, cb, out_ptr, d, d + t.rows, d + 2 * t.rows, d + 2 * t.rows + t.cols,
+                              d + 2 * t.rows + 2 * t.cols, d + 2 * t.rows + 2 * t.cols + t.K, t.rows, t.cols, t.K,
+                              st);
+      ++launches;
+      cur = op.out;
+      cur_ptr = out_ptr;
+      ping ^= 1;
+    }
+  }
+
+  // factor statistics (||A - A_prev||^2, ||A||^2, tr A^T L A) and E_k for
+  // factor k's current fp64 master (used after fctn_set_factors)
+  void factor_refresh(int k) {
+    const int64_t I = sh.dims[k], S = sh.s_of(k);
+    const double sgn = sign == FCTN_SIGN_PD ? -1.0 : 1.0;
+    launch_factor_colstats(A64[k], I, S, delta[k], sgn, colstats, st);
+    launch_factor_gram(A64[k], I, S, epart, E64[k], colstats, dstats + 3 * k, st);
+    launches += 3;
   }
 
   void configure(int dev, int dt, int n, const int64_t* dims, const int64_t* tri, const double* lm,
@@ -452,8 +546,11 @@ class Ctx : public Executor {
     cosT.assign(n, nullptr);
     sinT.assign(n, nullptr);
     check_mu.assign(n, NAN);
+    dft.clear();
     for (int k = 0; k < n; ++k) {
       int64_t I = sh.dims[k];
+      dft.push_back(plan_dft(I));
+      if (!dft.back().fast) throw UsageError("mode extent " + std::to_string(I) + " exceeds the on-chip DFT limit");
       std::vector<double> c(I), s(I), m(I / 2 + 1);
       double lmin = INFINITY;
       for (int64_t j = 0; j < I; ++j) {
@@ -485,41 +582,41 @@ class Ctx : public Executor {
     const int64_t I = sh.dims[k], S = sh.s_of(k), p = T / I;
     int64_t P = 1;
     for (int j = 0; j < k; ++j) P *= sh.dims[j];
+    // K2: Y_k = X_(k) M_k^T + rho A_prev (sylvester.py:104-106)
     StreamPlan sy = plan_stream(I, S, p, target_ctas());
-    StreamPlan sg = plan_stream(S, S, p, target_ctas());
     int pm = pbegin(FCTN_K_STREAM_Y);
     if (dtype == FCTN_F64)
       launch_stream<double>((const double*)X[cur], (const double*)Mbuf, ypart, I, P, S, p, sy, st);
     else
       launch_stream<float>((const float*)X[cur], (const float*)Mbuf, ypart, I, P, S, p, sy, st);
     pend(pm, (double)esize * (T + S * p), 1);
-    pm = pbegin(FCTN_K_GRAM);
-    if (dtype == FCTN_F64)
-      launch_stream<double>((const double*)Mbuf, (const double*)Mbuf, gpart, S, 1, S, p, sg, st);
-    else
-      launch_stream<float>((const float*)Mbuf, (const float*)Mbuf, gpart, S, 1, S, p, sg, st);
-    pend(pm, (double)esize * S * p, 1);
     pm = pbegin(FCTN_K_REDUCE);
-    launch_reduce_y(ypart, sy.nsplit, I, S, A64[k], rho, Y, st);
-    launch_reduce_g(gpart, sg.nsplit, S, G, st);
-    pend(pm, 8.0 * ((double)sy.nsplit * I * S + (double)sg.nsplit * S * S), 2);
-    pm = pbegin(FCTN_K_SOLVE);
+    launch_reduce_splits(ypart, sy.nsplit, I * S, A64[k], rho, Y, st);
+    pend(pm, 8.0 * ((double)sy.nsplit * I * S + 2.0 * I * S), 1);
+    // G_k = M_k M_k^T by the doubled network (sylvester.py:57-59)
+    pm = pbegin(FCTN_K_GRAM);
+    int64_t l0 = launches;
+    gram_network(k);
+    pend(pm, 8.0 * S * S, launches - l0);
     planner->meter.proj += 2 * I * p * S;   // sylvester.py:105
     planner->meter.gram += 2 * S * S * p;   // sylvester.py:58
-    const int64_t H1 = I / 2 + 1;
-    launch_dft_fwd(Y, I, S, cosT[k], sinT[k], Fr, Fi, st);
-    launch_chol_solve(G, S, H1, mu[k], Fr, Fi, check_mu[k], dstatus, st);
-    if (dtype == FCTN_F64)
-      launch_dft_inv<double>(Fr, Fi, I, S, cosT[k], sinT[k], A64[k], Ascratch, nullptr, extrap, alpha, beta, st);
-    else
-      launch_dft_inv<float>(Fr, Fi, I, S, cosT[k], sinT[k], A64[k], Ascratch, (float*)Ac[k], extrap, alpha, beta,
-                            st);
+    // K3: DFT along mode k, per-frequency SPD solves, inverse DFT (sylvester.py:108-116)
+    pm = pbegin(FCTN_K_SOLVE);
+    const DftPlan& dp = dft[k];
     const double sgn = sign == FCTN_SIGN_PD ? -1.0 : 1.0;
-    launch_factor_stats(Ascratch, A64[k], I, S, delta[k], sgn, dstats + 3 * k, st);
-    pend(pm, 8.0 * (4.0 * I * S + S * S), 4);
+    launch_dft_fwd(Y, dp, S, cosT[k], sinT[k], Fr, Fi, st);
+    launch_chol_solve(G, S, dp.H1, mu[k], Fr, Fi, check_mu[k], dstatus, st);
+    if (dtype == FCTN_F64)
+      launch_dft_inv<double>(Fr, Fi, dp, S, cosT[k], sinT[k], A64[k], Ascratch, nullptr, extrap, alpha, beta,
+                             delta[k], sgn, colstats, st);
+    else
+      launch_dft_inv<float>(Fr, Fi, dp, S, cosT[k], sinT[k], A64[k], Ascratch, (float*)Ac[k], extrap, alpha, beta,
+                            delta[k], sgn, colstats, st);
+    launch_factor_gram(Ascratch, I, S, epart, E64[k], colstats, dstats + 3 * k, st);
+    pend(pm, 8.0 * (4.0 * I * S + 2.0 * dp.H1 * S + S * S), 5);
     std::swap(A64[k], Ascratch);
     if (dtype == FCTN_F64) Ac[k] = A64[k];
-    launches += 9;
+    launches += 7;
     planner->versions[k] += 1;  // network.py:200
   }
 
@@ -634,9 +731,6 @@ class Ctx : public Executor {
     planner->partial_plain(0, this, M_ID);
     planner->meter = keep;
     compose(0, true);
-    const double sgn = sign == FCTN_SIGN_PD ? -1.0 : 1.0;
-    for (int k = 0; k < n; ++k)
-      launch_factor_stats(A64[k], A64[k], sh.dims[k], sh.s_of(k), delta[k], sgn, dstats + 3 * k, st);
     fetch_stats();
     double val = 0.5 * hstats[3 * n + 2];
     for (int k = 0; k < n; ++k) val += 0.5 * lam[k] * hstats[3 * k + 2];
@@ -715,6 +809,7 @@ int fctn_set_factors(fctn_ctx* c, const double* const* a_unf, const int64_t* ver
       if (x.dtype == FCTN_F32) fctn::launch_convert_f64_f32(x.A64[k], (float*)x.Ac[k], e, x.st);
       if (versions) x.planner->versions[k] = versions[k];
     }
+    for (int k = 0; k < x.sh.n; ++k) x.factor_refresh(k);
     if (reset_cache) x.planner->reset_cache(&x);
     CK(cudaStreamSynchronize(x.st));
   });

@@ -8,7 +8,8 @@
 
 namespace fctn {
 
-// K1: generic labeled contraction via offset tables (network.py:249-258,
+// ---------------------------------------------------------------- K1 merge
+// Generic labeled contraction via offset tables (network.py:249-258,
 // tensor.py:156-200).  C[rowC[r]+colC[c]] = sum_k A[rowA[r]+kA[k]] * B[colB[c]+kB[k]].
 template <typename T>
 void launch_contract(const T* A, const T* B, T* C, const int64_t* rowA, const int64_t* rowC,
@@ -24,14 +25,16 @@ struct PermDesc {
 template <typename T>
 void launch_permute(const T* in, T* out, const PermDesc& d, int64_t numel, cudaStream_t st);
 
-// K2: split-K streaming products over the long reduction axis p.
-//   part[split][i + I*s] = sum_{p in split} X(i,p) * M[s + S*p]
+void launch_convert_f64_f32(const double* in, float* out, int64_t n, cudaStream_t st);
+
+// ---------------------------------------------------------------- K2 stream
+// part[split][i + I*s] = sum_{p in split} X(i,p) * M[p + p_total*s]
 // with X(i,p) = X[(p%P) + P*i + P*I*(p/P)] (the mode-k view of an F-order
-// tensor; P = product of extents before mode k).  With X := M, I := S, P := 1
-// the same kernel yields the Gram partials.
+// tensor; P = product of extents before mode k).
 struct StreamPlan {
   int ts;        // padded s tile (16, 32, 64, 128)
-  int ti;        // i tile (4096 / ts)
+  int ri;        // rows of mode k per thread (1 or 4)
+  int ti;        // i tile
   int n_itiles;
   int nsplit;
   int64_t chunk; // p per split
@@ -40,31 +43,42 @@ StreamPlan plan_stream(int64_t I, int64_t S, int64_t p, int target_ctas);
 template <typename T>
 void launch_stream(const T* X, const T* M, double* part, int64_t I, int64_t P, int64_t S, int64_t p,
                    const StreamPlan& sp, cudaStream_t st);
-// Y[i+I*s] = sum_split part + rho * Aprev[i+I*s]   (sylvester.py:104-106)
-void launch_reduce_y(const double* part, int nsplit, int64_t I, int64_t S, const double* aprev,
-                     double rho, double* Y, cudaStream_t st);
-// G = sym(sum_split part)   (sylvester.py:57-59)
-void launch_reduce_g(const double* part, int nsplit, int64_t S, double* G, cudaStream_t st);
+// out[e] = sum_split part[split*n+e] + rho*aprev[e] (aprev may be null)   (sylvester.py:104-106)
+void launch_reduce_splits(const double* part, int nsplit, int64_t n, const double* aprev, double rho,
+                          double* out, cudaStream_t st);
+void launch_reduce_splits_f32(const float* part, int nsplit, int64_t n, const double* aprev, double rho,
+                              double* out, cudaStream_t st);
 
-// K3: the factor subproblem (sylvester.py:98-116) by real DFT along mode k
-// (L is circulant, laplacian.py:46-47,75-81) and one Cholesky solve of
-// (G + (lam*Lambda_w + rho) I) per frequency pair.
-void launch_dft_fwd(const double* Y, int64_t I, int64_t S, const double* cosT, const double* sinT,
+// ---------------------------------------------------------------- K3 solve
+struct DftPlan {
+  int64_t I, H1, I1, I2;
+  size_t smem;
+  bool fast;
+};
+DftPlan plan_dft(int64_t I);
+// F[w + H1*s] = sum_j Y[j + I*s] exp(-2 pi i w j / I), w < H1  (laplacian.py:75-81)
+void launch_dft_fwd(const double* Y, const DftPlan& p, int64_t S, const double* cosT, const double* sinT,
                     double* Fr, double* Fi, cudaStream_t st);
-// per-frequency solves; extra check CTA when check_mu is finite:
-// Cholesky of G + check_mu I must succeed (T-floor test, sylvester.py:108-113)
+// per-frequency Cholesky solves of (G + mu_w I) a_w = F_w; extra check CTA
+// when check_mu is finite (T-floor test, sylvester.py:108-113)
 void launch_chol_solve(const double* G, int64_t S, int64_t H1, const double* mu, double* Fr, double* Fi,
                        double check_mu, int* status, cudaStream_t st);
-// inverse DFT + extrapolation + factor write (solver.py:240-243,330-333)
+// inverse DFT + extrapolation + factor write + per-column stats
+// (solver.py:240-243,330-333; laplacian.py:59-71)
 template <typename T>
-void launch_dft_inv(const double* Fr, const double* Fi, int64_t I, int64_t S, const double* cosT,
-                    const double* sinT, const double* Aold, double* Anew, T* Acompute, int extrap,
-                    double alpha, double beta, cudaStream_t st);
-// ||A_new - A_old||^2, ||A_new||^2, tr(A^T L A) (laplacian.py:59-71) into out[0..2]
-void launch_factor_stats(const double* Anew, const double* Aold, int64_t I, int64_t S, double delta,
-                         double sgn, double* out, cudaStream_t st);
+void launch_dft_inv(const double* Fr, const double* Fi, const DftPlan& p, int64_t S, const double* cosT,
+                    const double* sinT, const double* Aold, double* Anew, T* Acompute, int extrap, double alpha,
+                    double beta, double delta, double sgn, double* colstats, cudaStream_t st);
+// per-column [0, ||a||^2, a.(L a)] without a previous iterate
+void launch_factor_colstats(const double* A, int64_t I, int64_t S, double delta, double sgn, double* colstats,
+                            cudaStream_t st);
+// E = A^T A (s x s) and the fold of colstats (S x 3) into stats3
+int fgram_splits(int64_t I);
+void launch_factor_gram(const double* A, int64_t I, int64_t S, double* part, double* E, const double* colstats,
+                        double* stats3, cudaStream_t st);
 
-// K4: C = A_(k) M (network.py:313-332) fused with the P_Omega blend
+// ---------------------------------------------------------------- K4 compose
+// C = A_(k) M (network.py:313-332) fused with the P_Omega blend
 // (solver.py:227-237) and the four sweep reductions (solver.py:220,346-354,382).
 // objective_only: no X_new write; sums (X - C)^2 into slot 2.
 template <typename T>
@@ -73,7 +87,5 @@ int launch_compose(const T* A, const T* M, const T* Xold, const uint8_t* mask, T
                    int64_t partial_cap, cudaStream_t st);
 // fixed-order final reduction of n x 4 partials into out[0..3]
 void launch_reduce4(const double* partials, int64_t n, double* out, cudaStream_t st);
-
-void launch_convert_f64_f32(const double* in, float* out, int64_t n, cudaStream_t st);
 
 }  // namespace fctn

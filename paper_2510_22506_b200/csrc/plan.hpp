@@ -14,6 +14,10 @@
 
 namespace fctn {
 
+// Primed labels (label + PRIME) name the second copy of a bond in the
+// doubled network E_j = A_(j)^T A_(j) used for the Gram of M_k.
+constexpr int PRIME = 1 << 16;
+
 struct Shape {
   int n = 0;
   std::vector<int64_t> dims;  // physical extents
@@ -24,7 +28,10 @@ struct Shape {
     return a * (n - 1) - a * (a - 1) / 2 + (b - a - 1);
   }
   int bond_label(int a, int b) const { return n + tri_index(a, b); }
-  int64_t extent(int label) const { return label < n ? dims[label] : tri[label - n]; }
+  int64_t extent(int label) const {
+    if (label >= PRIME) label -= PRIME;
+    return label < n ? dims[label] : tri[label - n];
+  }
   bool is_phys(int label) const { return label < n; }
   // bonds-to-k labels, ascending partner (rows of M_k / columns of A_(k))
   std::vector<int> bonds_of(int k) const {
@@ -56,13 +63,25 @@ struct Shape {
     for (int b : bonds_of(k)) out.push_back(b);
     return out;
   }
-  // M_k storage labels: [bonds to k ascending partner..., phys j != k ascending]
+  // M_k storage labels: [phys j != k ascending..., bonds to k ascending
+  // partner...]: p fastest, in X's own column order (network.py:360-371)
   std::vector<int> m_labels(int k) const {
-    std::vector<int> out = bonds_of(k);
+    std::vector<int> out;
     for (int j = 0; j < n; ++j)
       if (j != k) out.push_back(j);
+    for (int b : bonds_of(k)) out.push_back(b);
     return out;
   }
+  // E_j = A_(j)^T A_(j): [bonds of j..., primed bonds of j...]
+  std::vector<int> e_labels(int j) const {
+    std::vector<int> out = bonds_of_factor(j);
+    for (int b : bonds_of_factor(j)) out.push_back(b + PRIME);
+    return out;
+  }
+  // bonds of factor j in its unfolding's column order (ascending partner)
+  std::vector<int> bonds_of_factor(int j) const { return bonds_of(j); }
+  // G_k layout: [bonds to k..., primed bonds to k...] (s_k x s_k, column-major)
+  std::vector<int> g_labels(int k) const { return e_labels(k); }
 };
 
 // Reference FLOP meter labels (tensor.py:32-72).
