@@ -8,6 +8,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -361,7 +362,16 @@ class Ctx : public Executor {
     st = nullptr;
   }
 
-  int target_ctas() const { return 148 * 8; }
+  int target_ctas() const { return n_sm * 4; }
+  int n_sm = 148;
+  bool use_tc = true;  // fp32 K2 on tcgen05 (FCTN_NO_TC=1 forces the SIMT path)
+  bool tc_ok(int k) const {
+    if (dtype != FCTN_F32 || !use_tc) return false;
+    int64_t P = 1, Q = 1;
+    for (int j = 0; j < k; ++j) P *= sh.dims[j];
+    for (int j = k + 1; j < sh.n; ++j) Q *= sh.dims[j];
+    return tc_stream_supported(sh.dims[k], P, Q, sh.s_of(k));
+  }
 
   void configure_shape() {
     // (re)allocate everything whose size depends on the rank table
@@ -378,6 +388,12 @@ class Ctx : public Executor {
       max_h = std::max(max_h, (I / 2 + 1) * S);
       StreamPlan sy = plan_stream(I, S, p, target_ctas());
       max_yp = std::max(max_yp, (int64_t)sy.nsplit * I * S);
+      if (tc_ok(k)) {
+        int64_t P = 1;
+        for (int j = 0; j < k; ++j) P *= sh.dims[j];
+        TcStreamPlan tp = plan_stream_tc(I, P, p / P, S, n_sm);
+        max_yp = std::max(max_yp, (tp.nsplit * I * S + 1) / 2);  // float partials in the double buffer
+      }
       max_part = std::max(max_part, ((I + 63) / 64) * ((p + 63) / 64));
       max_ep = std::max(max_ep, (int64_t)fgram_splits(I) * S * S);
     }
@@ -523,6 +539,11 @@ class Ctx : public Executor {
     alg = a;
     budget = bud;
     CK(cudaSetDevice(device));
+    CK(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, device));
+    {
+      const char* e = getenv("FCTN_NO_TC");
+      use_tc = !(e && e[0] == '1');
+    }
     CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
     CK(cudaEventCreate(&ev0));
     CK(cudaEventCreate(&ev1));
@@ -583,16 +604,28 @@ class Ctx : public Executor {
     int64_t P = 1;
     for (int j = 0; j < k; ++j) P *= sh.dims[j];
     // K2: Y_k = X_(k) M_k^T + rho A_prev (sylvester.py:104-106)
-    StreamPlan sy = plan_stream(I, S, p, target_ctas());
     int pm = pbegin(FCTN_K_STREAM_Y);
-    if (dtype == FCTN_F64)
-      launch_stream<double>((const double*)X[cur], (const double*)Mbuf, ypart, I, P, S, p, sy, st);
-    else
-      launch_stream<float>((const float*)X[cur], (const float*)Mbuf, ypart, I, P, S, p, sy, st);
+    int nsplit = 0;
+    const bool tc = tc_ok(k);
+    if (tc) {
+      TcStreamPlan tp = plan_stream_tc(I, P, p / P, S, n_sm);
+      launch_stream_tc((const float*)X[cur], (const float*)Mbuf, (float*)ypart, I, P, p / P, S, tp, st);
+      nsplit = (int)tp.nsplit;
+    } else {
+      StreamPlan sy = plan_stream(I, S, p, target_ctas());
+      if (dtype == FCTN_F64)
+        launch_stream<double>((const double*)X[cur], (const double*)Mbuf, ypart, I, P, S, p, sy, st);
+      else
+        launch_stream<float>((const float*)X[cur], (const float*)Mbuf, ypart, I, P, S, p, sy, st);
+      nsplit = sy.nsplit;
+    }
     pend(pm, (double)esize * (T + S * p), 1);
     pm = pbegin(FCTN_K_REDUCE);
-    launch_reduce_splits(ypart, sy.nsplit, I * S, A64[k], rho, Y, st);
-    pend(pm, 8.0 * ((double)sy.nsplit * I * S + 2.0 * I * S), 1);
+    if (tc)
+      launch_reduce_splits_f32((const float*)ypart, nsplit, I * S, A64[k], rho, Y, st);
+    else
+      launch_reduce_splits(ypart, nsplit, I * S, A64[k], rho, Y, st);
+    pend(pm, (tc ? 4.0 : 8.0) * nsplit * I * S + 16.0 * I * S, 1);
     // G_k = M_k M_k^T by the doubled network (sylvester.py:57-59)
     pm = pbegin(FCTN_K_GRAM);
     int64_t l0 = launches;

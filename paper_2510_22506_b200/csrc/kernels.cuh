@@ -49,6 +49,20 @@ void launch_reduce_splits(const double* part, int nsplit, int64_t n, const doubl
 void launch_reduce_splits_f32(const float* part, int nsplit, int64_t n, const double* aprev, double rho,
                               double* out, cudaStream_t st);
 
+// tcgen05 TF32 path (stream_tc.cu): fp32 partials part[split][i + I*s]
+struct TcStreamPlan {
+  int nt;              // UMMA N (bond tile, padded S)
+  int64_t n_mtiles;    // 128-row tiles of mode k
+  int64_t npb;         // 32-wide K blocks per run of the fastest mode (1 when P == 1)
+  int64_t nkb;         // K blocks in total
+  int64_t kb_per_split;
+  int64_t nsplit;
+};
+bool tc_stream_supported(int64_t I, int64_t P, int64_t Q, int64_t S);
+TcStreamPlan plan_stream_tc(int64_t I, int64_t P, int64_t Q, int64_t S, int n_sm);
+void launch_stream_tc(const float* X, const float* M, float* part, int64_t I, int64_t P, int64_t Q, int64_t S,
+                      const TcStreamPlan& tp, cudaStream_t st);
+
 // ---------------------------------------------------------------- K3 solve
 struct DftPlan {
   int64_t I, H1, I1, I2;

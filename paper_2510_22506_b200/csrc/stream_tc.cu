@@ -1,0 +1,239 @@
+// K2 on the B200 tensor cores (fp32 data, tcgen05 kind::tf32, fp32
+// accumulation in TMEM): Y_k partials = X_(k) M_k^T (sylvester.py:104).
+//
+// One CTA = one 128-row tile of mode k x one split of the reduction axis p.
+// Warp roles (192 threads):
+//   warp 0      TMA producer: X tile (128 x 32 fp32) + M tile (NT x 32) per stage
+//   warp 1      TMEM allocator + single-thread MMA issuer (4 x K=8 per stage)
+//   warps 2..5  epilogue: tcgen05.ld the 128 x NT accumulator, write fp32 partials
+// X is read in place through a TMA descriptor of the mode-k view:
+//   P > 1  (modes before k exist): 3-D [P, I, Q], K-major A tile (rows = i,
+//          128 B = 32 consecutive p along the fastest mode)
+//   P == 1 (k = 0): 2-D [I, Q], MN-major A tile (i contiguous), four 32-row
+//          boxes per 128-row tile
+// M_k (p-fastest) is a 3-D [P, Q, S] (or 2-D [Q, S]) K-major B tile.  Both
+// use SWIZZLE_128B; OOB boxes are zero-filled by TMA, so ragged P, I, S need
+// no special casing.  Partials are combined by the fixed-order split reduce.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_runtime.h>
+
+#include <stdexcept>
+#include <string>
+
+#include "kernels.cuh"
+#include "tc_common.cuh"
+
+namespace fctn {
+
+namespace {
+
+constexpr int BK = 32;  // fp32 per 128-byte row
+constexpr int STAGES = 6;
+constexpr int A_BYTES = 128 * BK * 4;  // 16 KB
+
+template <int NT>
+struct StreamSmem {
+  static constexpr int B_BYTES = NT * BK * 4;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int TOTAL = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+};
+
+template <int NT, bool AMN>
+__global__ void __launch_bounds__(192, 1)
+    k_stream_tc(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmM,
+                float* __restrict__ part, int I, int S, long long nkb_total, long long kb_per_split, int nPB) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES * A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * StreamSmem<NT>::STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tmem_full = empty + STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int mtile = blockIdx.x;
+  const long long split = blockIdx.y;
+  const long long kb0 = split * kb_per_split;
+  long long kb1 = kb0 + kb_per_split;
+  if (kb1 > nkb_total) kb1 = nkb_total;
+  const int nkb = (int)(kb1 - kb0);
+  constexpr int NCOLS = NT <= 32 ? 32 : NT <= 64 ? 64 : NT <= 128 ? 128 : 256;
+
+  if (warp == 0 && lane == 0) {
+    tc::tma_prefetch(&tmX);
+    tc::tma_prefetch(&tmM);
+    for (int s = 0; s < STAGES; ++s) {
+      tc::mbar_init(&full[s], 1);
+      tc::mbar_init(&empty[s], 1);
+    }
+    tc::mbar_init(tmem_full, 1);
+    tc::fence_barrier_init();
+  }
+  if (warp == 1) tc::tmem_alloc<NCOLS>(tmem_slot);
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0 && lane == 0) {
+    // ---------------- TMA producer
+    const int i0 = mtile * 128;
+    for (int it = 0; it < nkb; ++it) {
+      const int s = it % STAGES;
+      const uint32_t ph = (it / STAGES) & 1;
+      tc::mbar_wait(&empty[s], ph ^ 1);
+      tc::mbar_expect_tx(&full[s], StreamSmem<NT>::STAGE_BYTES);
+      const long long kb = kb0 + it;
+      uint8_t* a = sA + s * A_BYTES;
+      uint8_t* b = sB + s * StreamSmem<NT>::B_BYTES;
+      if (AMN) {
+        const int q0 = (int)(kb * BK);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) tc::tma_load_2d(a + c * 4096, &tmX, &full[s], i0 + 32 * c, q0);
+        tc::tma_load_2d(b, &tmM, &full[s], q0, 0);
+      } else {
+        const int pb = (int)(kb % nPB) * BK;
+        const int q = (int)(kb / nPB);
+        tc::tma_load_3d(a, &tmX, &full[s], pb, i0, q);
+        tc::tma_load_3d(b, &tmM, &full[s], pb, q, 0);
+      }
+    }
+  } else if (warp == 1 && lane == 0) {
+    // ---------------- MMA issuer
+    constexpr uint32_t idesc = tc::idesc_tf32(128, NT, AMN, false);
+    for (int it = 0; it < nkb; ++it) {
+      const int s = it % STAGES;
+      const uint32_t ph = (it / STAGES) & 1;
+      tc::mbar_wait(&full[s], ph);
+      tc::fence_after_sync();
+      const uint32_t a = tc::smem_u32(sA + s * A_BYTES);
+      const uint32_t b = tc::smem_u32(sB + s * StreamSmem<NT>::B_BYTES);
+#pragma unroll
+      for (int kk = 0; kk < BK / 8; ++kk) {
+        const uint64_t ad = AMN ? tc::sdesc(a + kk * 1024, 4096, 1024) : tc::sdesc(a + kk * 32, 16, 1024);
+        const uint64_t bd = tc::sdesc(b + kk * 32, 16, 1024);
+        tc::mma_tf32(tmem, ad, bd, idesc, (it | kk) != 0);
+      }
+      tc::mma_commit(&empty[s]);
+    }
+    tc::mma_commit(tmem_full);
+  } else if (warp >= 2) {
+    // ---------------- epilogue
+    tc::mbar_wait(tmem_full, 0);
+    tc::fence_after_sync();
+    const int q = warp & 3;
+    const int row = 32 * q + lane;
+    const long long i = (long long)mtile * 128 + row;
+    float* out = part + split * (long long)I * S;
+#pragma unroll 1
+    for (int c0 = 0; c0 < NT; c0 += 16) {
+      float v[16];
+      tc::tmem_ld16(tmem + ((uint32_t)(32 * q) << 16) + c0, v);
+      if (i < I) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const int s = c0 + j;
+          if (s < S) out[i + (long long)I * s] = v[j];
+        }
+      }
+    }
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  if (warp == 1) {
+    tc::fence_after_sync();
+    tc::tmem_dealloc<NCOLS>(tmem);
+  }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q);
+    if (e != cudaSuccess || q != cudaDriverEntryPointSuccess || !p)
+      throw std::runtime_error("cuTensorMapEncodeTiled is unavailable");
+    fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+CUtensorMap make_map(const void* base, int rank, const uint64_t* dims, const uint64_t* strides_bytes,
+                     const uint32_t* box) {
+  CUtensorMap m;
+  uint32_t es[5] = {1, 1, 1, 1, 1};
+  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, (cuuint32_t)rank, const_cast<void*>(base),
+                           (const cuuint64_t*)dims, (const cuuint64_t*)strides_bytes, (const cuuint32_t*)box,
+                           (const cuuint32_t*)es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw std::runtime_error("cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+  return m;
+}
+
+template <int NT, bool AMN>
+void go(const CUtensorMap& mx, const CUtensorMap& mm, float* part, int64_t I, int64_t S, const TcStreamPlan& tp,
+        cudaStream_t st) {
+  const int smem = StreamSmem<NT>::TOTAL;
+  auto fn = k_stream_tc<NT, AMN>;
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) throw std::runtime_error(std::string("stream_tc smem: ") + cudaGetErrorString(e));
+  dim3 grid((unsigned)tp.n_mtiles, (unsigned)tp.nsplit);
+  fn<<<grid, 192, smem, st>>>(mx, mm, part, (int)I, (int)S, tp.nkb, tp.kb_per_split, (int)tp.npb);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) throw std::runtime_error(std::string("stream_tc: ") + cudaGetErrorString(e));
+}
+
+}  // namespace
+
+bool tc_stream_supported(int64_t I, int64_t P, int64_t Q, int64_t S) {
+  if (S > 128) return false;
+  if (I > (1LL << 31) || Q > (1LL << 31) || P > (1LL << 31)) return false;
+  if (P == 1) return (I % 4 == 0) && (Q % 4 == 0);
+  return P % 4 == 0;
+}
+
+TcStreamPlan plan_stream_tc(int64_t I, int64_t P, int64_t Q, int64_t S, int n_sm) {
+  TcStreamPlan tp;
+  tp.nt = S <= 32 ? 32 : S <= 64 ? 64 : S <= 96 ? 96 : 128;
+  tp.n_mtiles = (I + 127) / 128;
+  tp.npb = P == 1 ? 1 : (P + BK - 1) / BK;
+  tp.nkb = P == 1 ? (Q + BK - 1) / BK : tp.npb * Q;
+  int64_t want = n_sm / tp.n_mtiles;
+  if (want < 1) want = 1;
+  if (want > tp.nkb) want = tp.nkb;
+  tp.kb_per_split = (tp.nkb + want - 1) / want;
+  tp.nsplit = (tp.nkb + tp.kb_per_split - 1) / tp.kb_per_split;
+  return tp;
+}
+
+void launch_stream_tc(const float* X, const float* M, float* part, int64_t I, int64_t P, int64_t Q, int64_t S,
+                      const TcStreamPlan& tp, cudaStream_t st) {
+  CUtensorMap mx, mm;
+  if (P == 1) {
+    uint64_t dx[2] = {(uint64_t)I, (uint64_t)Q}, sx[1] = {(uint64_t)I * 4};
+    uint32_t bx[2] = {32, 32};
+    mx = make_map(X, 2, dx, sx, bx);
+    uint64_t dm[2] = {(uint64_t)Q, (uint64_t)S}, sm[1] = {(uint64_t)Q * 4};
+    uint32_t bm[2] = {32, (uint32_t)tp.nt};
+    mm = make_map(M, 2, dm, sm, bm);
+  } else {
+    uint64_t dx[3] = {(uint64_t)P, (uint64_t)I, (uint64_t)Q}, sx[2] = {(uint64_t)P * 4, (uint64_t)P * I * 4};
+    uint32_t bx[3] = {32, 128, 1};
+    mx = make_map(X, 3, dx, sx, bx);
+    uint64_t dm[3] = {(uint64_t)P, (uint64_t)Q, (uint64_t)S}, sm[2] = {(uint64_t)P * 4, (uint64_t)P * Q * 4};
+    uint32_t bm[3] = {32, 1, (uint32_t)tp.nt};
+    mm = make_map(M, 3, dm, sm, bm);
+  }
+  const bool amn = P == 1;
+  switch (tp.nt) {
+    case 32: amn ? go<32, true>(mx, mm, part, I, S, tp, st) : go<32, false>(mx, mm, part, I, S, tp, st); break;
+    case 64: amn ? go<64, true>(mx, mm, part, I, S, tp, st) : go<64, false>(mx, mm, part, I, S, tp, st); break;
+    case 96: amn ? go<96, true>(mx, mm, part, I, S, tp, st) : go<96, false>(mx, mm, part, I, S, tp, st); break;
+    default: amn ? go<128, true>(mx, mm, part, I, S, tp, st) : go<128, false>(mx, mm, part, I, S, tp, st); break;
+  }
+}
+
+}  // namespace fctn
