@@ -123,6 +123,14 @@ int fctn_nccl_unique_id(uint8_t* id128);
 int fctn_set_comm(fctn_ctx* ctx, const uint8_t* id128, int rank, int nranks, int64_t slab_lo,
                   int64_t slab_hi);
 
+/* Kernel self-test (tests only): Y = X_(k) M^T for a mode-k view X of
+ * extents [P, I, Q] (first fastest) and a p-fastest M (p = P*Q, S rows),
+ * through the K2 path the context would use (tcgen05 TF32 when use_tc and
+ * dtype is FCTN_F32 and TMA can describe the view, else SIMT).  Host
+ * buffers; Y is I x S column-major float64. */
+int fctn_selftest_stream(int device, int dtype, int use_tc, int64_t I, int64_t P, int64_t Q, int64_t S,
+                         const void* x, const void* m, double* y);
+
 /* Sync the context stream. */
 int fctn_sync(fctn_ctx* ctx);
 

@@ -24,7 +24,7 @@ CT_FLOPS, CT_MK, CT_COMPOSE, CT_HITS, CT_LAUNCHES, CT_COUNT = 0, 1, 2, 3, 4, 8
 EXPORTS = [
     "fctn_create", "fctn_upload", "fctn_set_factors", "fctn_set_rank", "fctn_get_factors", "fctn_get_x",
     "fctn_objective", "fctn_sweep", "fctn_plan_sweeps", "fctn_nccl_unique_id", "fctn_set_comm",
-    "fctn_sync", "fctn_timer", "fctn_set_profiling", "fctn_get_profile", "fctn_last_error", "fctn_version",
+    "fctn_sync", "fctn_selftest_stream", "fctn_timer", "fctn_set_profiling", "fctn_get_profile", "fctn_last_error", "fctn_version",
     "fctn_destroy",
 ]
 K_CLASSES = ["merge", "stream_y", "gram", "reduce", "solve", "compose", "k6", "k7"]
@@ -61,6 +61,8 @@ def lib():
     L.fctn_nccl_unique_id.argtypes = [P]
     L.fctn_set_comm.argtypes = [P, P, C.c_int, C.c_int, C.c_int64, C.c_int64]
     L.fctn_sync.argtypes = [P]
+    L.fctn_selftest_stream.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int64, C.c_int64, C.c_int64, C.c_int64, P, P,
+                                       f64p]
     L.fctn_timer.argtypes = [P, C.c_int, f64p]
     L.fctn_set_profiling.argtypes = [P, C.c_int]
     L.fctn_get_profile.argtypes = [P, f64p, i64p, f64p]
@@ -111,6 +113,25 @@ def plan_sweeps(dims, rank_tri, algorithm: int, cache_budget: int, orders) -> np
                                 out.ctypes.data_as(C.POINTER(C.c_int64)))
     check(rc)
     return out
+
+
+def selftest_stream(x, m, k, use_tc=True, device=0):
+    """Y = X_(k) M^T through the library's K2 path (kernel unit tests).
+    x: F-order tensor (float32 or float64); m: (p, S) F-order with p in X's
+    column order (modes before k fastest)."""
+    dt = F32 if x.dtype == np.float32 else F64
+    x = np.asfortranarray(x)
+    m = np.asfortranarray(m, dtype=x.dtype)
+    dims = x.shape
+    I = dims[k]
+    P = int(np.prod(dims[:k])) if k > 0 else 1
+    Q = int(np.prod(dims[k + 1:])) if k + 1 < len(dims) else 1
+    S = m.shape[1]
+    y = np.zeros((I, S), dtype=np.float64, order="F")
+    rc = lib().fctn_selftest_stream(int(device), dt, int(bool(use_tc)), I, P, Q, S, x.ctypes.data_as(C.c_void_p),
+                                    m.ctypes.data_as(C.c_void_p), y.ctypes.data_as(C.POINTER(C.c_double)))
+    check(rc)
+    return y
 
 
 class Context:

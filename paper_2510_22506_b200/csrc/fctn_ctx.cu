@@ -983,6 +983,47 @@ int fctn_get_profile(fctn_ctx* c, double* ms, int64_t* launches, double* bytes) 
   });
 }
 
+int fctn_selftest_stream(int device, int dtype, int use_tc, int64_t I, int64_t P, int64_t Q, int64_t S,
+                         const void* x, const void* m, double* y) {
+  return fctn::guarded(nullptr, [&] {
+    CK(cudaSetDevice(device));
+    cudaStream_t st;
+    CK(cudaStreamCreate(&st));
+    const size_t es = dtype == FCTN_F64 ? 8 : 4;
+    const int64_t T = I * P * Q, p = P * Q;
+    void *dx, *dm;
+    double *part, *dy;
+    int nsm = 148;
+    CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device));
+    CK(cudaMalloc(&dx, T * es));
+    CK(cudaMalloc(&dm, p * S * es));
+    CK(cudaMalloc(&dy, I * S * sizeof(double)));
+    CK(cudaMemcpy(dx, x, T * es, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(dm, m, p * S * es, cudaMemcpyHostToDevice));
+    if (use_tc && dtype == FCTN_F32 && fctn::tc_stream_supported(I, P, Q, S)) {
+      fctn::TcStreamPlan tp = fctn::plan_stream_tc(I, P, Q, S, nsm);
+      CK(cudaMalloc(&part, tp.nsplit * I * S * sizeof(float)));
+      fctn::launch_stream_tc((const float*)dx, (const float*)dm, (float*)part, I, P, Q, S, tp, st);
+      fctn::launch_reduce_splits_f32((const float*)part, (int)tp.nsplit, I * S, nullptr, 0.0, dy, st);
+    } else {
+      fctn::StreamPlan sp = fctn::plan_stream(I, S, p, nsm * 4);
+      CK(cudaMalloc(&part, (int64_t)sp.nsplit * I * S * sizeof(double)));
+      if (dtype == FCTN_F64)
+        fctn::launch_stream<double>((const double*)dx, (const double*)dm, part, I, P, S, p, sp, st);
+      else
+        fctn::launch_stream<float>((const float*)dx, (const float*)dm, part, I, P, S, p, sp, st);
+      fctn::launch_reduce_splits(part, sp.nsplit, I * S, nullptr, 0.0, dy, st);
+    }
+    CK(cudaStreamSynchronize(st));
+    CK(cudaMemcpy(y, dy, I * S * sizeof(double), cudaMemcpyDeviceToHost));
+    cudaFree(dx);
+    cudaFree(dm);
+    cudaFree(dy);
+    cudaFree(part);
+    cudaStreamDestroy(st);
+  });
+}
+
 int fctn_sync(fctn_ctx* c) {
   return fctn::guarded(&c->impl, [&] { CK(cudaStreamSynchronize(c->impl.st)); });
 }

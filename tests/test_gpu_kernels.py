@@ -1,0 +1,42 @@
+"""GPU unit tests of single kernels through the C ABI self-test entry points
+(each against a numpy fp64 product of the same inputs)."""
+import numpy as np
+import pytest
+
+from paper_2510_22506_b200 import _native
+
+pytestmark = pytest.mark.gpu
+
+
+def _unfold(x, k):
+    rest = [m for m in range(x.ndim) if m != k]
+    return np.transpose(x, [k] + rest).reshape((x.shape[k], -1), order="F")
+
+
+@pytest.mark.parametrize("dims,k,S", [
+    ((256, 64, 8), 0, 64), ((256, 64, 8), 1, 64), ((256, 64, 8), 2, 64),
+    ((48, 40, 36), 0, 81), ((48, 40, 36), 1, 27), ((48, 40, 36), 2, 9),
+    ((2048, 32, 4), 0, 64), ((20, 20, 20, 20), 3, 27),
+])
+@pytest.mark.parametrize("use_tc", [True, False])
+def test_stream_fp32_matches_numpy(dims, k, S, use_tc):
+    rng = np.random.default_rng(3)
+    x = np.asfortranarray(rng.standard_normal(dims).astype(np.float32))
+    p = int(np.prod(dims)) // dims[k]
+    m = np.asfortranarray(rng.standard_normal((p, S)).astype(np.float32))
+    ref = _unfold(x.astype(np.float64), k) @ m.astype(np.float64)
+    y = _native.selftest_stream(x, m, k, use_tc=use_tc)
+    err = np.linalg.norm(y - ref) / np.linalg.norm(ref)
+    # TF32 inputs (10-bit mantissa): ~1e-3 relative for random data
+    assert err <= (3e-3 if use_tc else 1e-5), err
+
+
+@pytest.mark.parametrize("dims,k,S", [((30, 20, 10), 0, 16), ((30, 20, 10), 1, 36), ((7, 9, 5, 6), 2, 125)])
+def test_stream_fp64_matches_numpy(dims, k, S):
+    rng = np.random.default_rng(4)
+    x = np.asfortranarray(rng.standard_normal(dims))
+    p = int(np.prod(dims)) // dims[k]
+    m = np.asfortranarray(rng.standard_normal((p, S)))
+    ref = _unfold(x, k) @ m
+    y = _native.selftest_stream(x, m, k)
+    assert np.linalg.norm(y - ref) / np.linalg.norm(ref) <= 1e-13
