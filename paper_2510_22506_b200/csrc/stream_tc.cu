@@ -10,13 +10,15 @@
 //   P > 1  (modes before k exist): 3-D [P, I, Q], K-major A tile (rows = i,
 //          128 B = 32 consecutive p along the fastest mode)
 //   P == 1 (k = 0): 2-D [I, Q], MN-major A tile (i contiguous), four 32-row
-//          boxes per 128-row tile
+//          boxes per 128-row tile, SWIZZLE_128B with 32-byte atoms (the only
+//          MN-major smem layout UMMA accepts for 32-bit operands)
 // M_k (p-fastest) is a 3-D [P, Q, S] (or 2-D [Q, S]) K-major B tile.  Both
 // use SWIZZLE_128B; OOB boxes are zero-filled by TMA, so ragged P, I, S need
 // no special casing.  Partials are combined by the fixed-order split reduce.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
+
 
 #include <stdexcept>
 #include <string>
@@ -112,7 +114,7 @@ __global__ void __launch_bounds__(192, 1)
       const uint32_t b = tc::smem_u32(sB + s * StreamSmem<NT>::B_BYTES);
 #pragma unroll
       for (int kk = 0; kk < BK / 8; ++kk) {
-        const uint64_t ad = AMN ? tc::sdesc(a + kk * 1024, 4096, 1024) : tc::sdesc(a + kk * 32, 16, 1024);
+        const uint64_t ad = AMN ? tc::sdesc(a + kk * 1024, 4096, 512, 1) : tc::sdesc(a + kk * 32, 16, 1024);
         const uint64_t bd = tc::sdesc(b + kk * 32, 16, 1024);
         tc::mma_tf32(tmem, ad, bd, idesc, (it | kk) != 0);
       }
@@ -162,12 +164,12 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 }
 
 CUtensorMap make_map(const void* base, int rank, const uint64_t* dims, const uint64_t* strides_bytes,
-                     const uint32_t* box) {
+                     const uint32_t* box, CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
   CUtensorMap m;
   uint32_t es[5] = {1, 1, 1, 1, 1};
   CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, (cuuint32_t)rank, const_cast<void*>(base),
                            (const cuuint64_t*)dims, (const cuuint64_t*)strides_bytes, (const cuuint32_t*)box,
-                           (const cuuint32_t*)es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           (const cuuint32_t*)es, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) throw std::runtime_error("cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
   return m;
@@ -215,7 +217,7 @@ void launch_stream_tc(const float* X, const float* M, float* part, int64_t I, in
   if (P == 1) {
     uint64_t dx[2] = {(uint64_t)I, (uint64_t)Q}, sx[1] = {(uint64_t)I * 4};
     uint32_t bx[2] = {32, 32};
-    mx = make_map(X, 2, dx, sx, bx);
+    mx = make_map(X, 2, dx, sx, bx, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);  // MN-major tf32: 32-B atoms
     uint64_t dm[2] = {(uint64_t)Q, (uint64_t)S}, sm[1] = {(uint64_t)Q * 4};
     uint32_t bm[2] = {32, (uint32_t)tp.nt};
     mm = make_map(M, 2, dm, sm, bm);

@@ -68,13 +68,16 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* m, uin
 //  K-major: rows of 128 B (32 fp32 along K), 8-row groups at SBO = 1024 B.
 //  MN-major: 128-B rows along MN, K rows at 128 B, K 8-groups at SBO,
 //            MN 32-element chunks at LBO.
-__device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo_bytes, uint32_t sbo_bytes) {
+//  MN-major 32-bit (tf32) operands must use SWIZZLE_128B_BASE32B (layout 1):
+//            32-B chunks XOR-ed with the K row (mod 4), K groups of 4 rows.
+__device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo_bytes, uint32_t sbo_bytes,
+                                          uint32_t layout = 2) {
   uint64_t d = 0;
   d |= (uint64_t)((saddr >> 4) & 0x3FFF);
   d |= (uint64_t)((lbo_bytes >> 4) & 0x3FFF) << 16;
   d |= (uint64_t)((sbo_bytes >> 4) & 0x3FFF) << 32;
   d |= (uint64_t)1 << 46;  // version (sm100)
-  d |= (uint64_t)2 << 61;  // SWIZZLE_128B
+  d |= (uint64_t)layout << 61;  // 2 = SWIZZLE_128B, 1 = SWIZZLE_128B_BASE32B
   return d;
 }
 // Instruction descriptor: kind::tf32, fp32 accumulate.
