@@ -71,6 +71,7 @@ class Ctx : public Executor {
   void* X[2] = {nullptr, nullptr};
   int cur = 0;
   uint8_t* mask = nullptr;
+  uint32_t* maskbits = nullptr;  // 1 bit per entry (TC compose epilogue)
   std::vector<double*> A64;
   std::vector<void*> Ac;  // compute copy (== A64 for fp64)
   double* Ascratch = nullptr;
@@ -347,6 +348,8 @@ class Ctx : public Executor {
     cudaFree(X[0]);
     cudaFree(X[1]);
     cudaFree(mask);
+    cudaFree(maskbits);
+    maskbits = nullptr;
     cudaFree(dstats);
     cudaFree(dstatus);
     if (hstats) cudaFreeHost(hstats);
@@ -422,7 +425,7 @@ class Ctx : public Executor {
     CK(cudaMalloc(&ypart, max_yp * sizeof(double)));
     CK(cudaMalloc(&epart, max_ep * sizeof(double)));
     CK(cudaMalloc(&colstats, max_s * 3 * sizeof(double)));
-    partial_cap = max_part;
+    partial_cap = std::max<int64_t>(max_part, 4 * n_sm);
     CK(cudaMalloc(&partials, max_part * 4 * sizeof(double)));
     int64_t gcap = max_ss;
     for (int k = 0; k < n; ++k) gcap = std::max(gcap, gram_network_peak(k));
@@ -557,6 +560,7 @@ class Ctx : public Executor {
     CK(cudaMalloc(&X[0], T * esize));
     CK(cudaMalloc(&X[1], T * esize));
     CK(cudaMalloc(&mask, T));
+    CK(cudaMalloc(&maskbits, ((T + 31) / 32) * sizeof(uint32_t)));
     CK(cudaMalloc(&dstats, (n * 3 + 8) * sizeof(double)));
     CK(cudaMalloc(&dstatus, sizeof(int)));
     CK(cudaMemset(dstatus, 0, sizeof(int)));
@@ -660,7 +664,10 @@ class Ctx : public Executor {
     for (int j = 0; j < k; ++j) P *= sh.dims[j];
     int nb;
     int pm = pbegin(FCTN_K_COMPOSE);
-    if (dtype == FCTN_F64)
+    if (dtype == FCTN_F32 && use_tc && tc_compose_supported(I, P, p, S))
+      nb = launch_compose_tc((const float*)Ac[k], (const float*)Mbuf, (const float*)X[cur], maskbits,
+                             (float*)X[cur ^ 1], I, P, S, p, rho, objective_only, partials, partial_cap, n_sm, st);
+    else if (dtype == FCTN_F64)
       nb = launch_compose<double>((const double*)Ac[k], (const double*)Mbuf, (const double*)X[cur], mask,
                                   (double*)X[cur ^ 1], I, P, S, p, rho, objective_only, partials, partial_cap, st);
     else
@@ -827,6 +834,7 @@ int fctn_upload(fctn_ctx* c, const void* x_F, const uint8_t* mask_F) {
     const int64_t T = x.sh.total();
     CK(cudaMemcpyAsync(x.X[0], x_F, T * x.esize, cudaMemcpyHostToDevice, x.st));
     CK(cudaMemcpyAsync(x.mask, mask_F, T, cudaMemcpyHostToDevice, x.st));
+    fctn::launch_pack_mask(x.mask, T, x.maskbits, x.st);
     CK(cudaStreamSynchronize(x.st));
     x.cur = 0;
     x.uploaded = true;
