@@ -10,8 +10,9 @@
 // atoms) with K = s.  Persistent CTAs (one per SM) walk the tiles with a
 // 2-stage smem ring and a double-buffered TMEM accumulator, so the MMA of
 // tile t+1 overlaps the epilogue of tile t.
-// Warp roles (320 threads): warp 0 TMA, warp 1 TMEM alloc + MMA issue,
-// warps 2..9 epilogue (two warps per TMEM lane quadrant, column halves).
+// Warp roles (448 threads): warp 0 TMA, warp 1 TMEM alloc + MMA issue,
+// warps 2..5 TF32 rounding / 3xTF32 split of the landed operand tiles,
+// warps 6..13 epilogue (two warps per TMEM lane quadrant, column halves).
 // The observation mask is read bit-packed (1 bit per entry, F order).
 #include <cuda.h>
 #include <cudaTypedefs.h>
@@ -31,8 +32,10 @@ CUtensorMap tc_make_map_f32(const void* base, int rank, const uint64_t* dims, co
 
 namespace {
 
+constexpr int CONV_WARPS = 4;
 constexpr int EPI_WARPS = 8;
-constexpr int THREADS = 64 + 32 * EPI_WARPS;
+constexpr int EPI0 = 2 + CONV_WARPS;  // first epilogue warp
+constexpr int THREADS = 32 * (EPI0 + EPI_WARPS);
 
 struct ComposeArgs {
   const float* Xo;
@@ -48,7 +51,7 @@ struct ComposeArgs {
   int objective_only;
 };
 
-template <int N>
+template <int N, bool SPLIT>
 __global__ void __launch_bounds__(THREADS, 1)
     k_compose_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                  const ComposeArgs args) {
@@ -56,11 +59,13 @@ __global__ void __launch_bounds__(THREADS, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int kp = args.kp;
   const uint32_t a_bytes = 128u * kp * 4u, b_bytes = (uint32_t)N * kp * 4u;
-  const uint32_t stage_bytes = a_bytes + b_bytes;
+  const uint32_t tma_bytes = a_bytes + b_bytes;
+  const uint32_t stage_bytes = tma_bytes * (SPLIT ? 2 : 1);  // [A hi | B hi | (A lo | B lo)]
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + 2 * stage_bytes);
-  uint64_t* empty = full + 2;
+  uint64_t* conv = full + 2;
+  uint64_t* empty = conv + 2;
   uint64_t* tfull = empty + 2;
-  uint64_t* tempty = tfull + 2;
+  uint64_t* tempty = tfull + 2;  // (barrier block: 10 x 8 B)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
   __shared__ double red[4][THREADS];
 
@@ -72,6 +77,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     tc::tma_prefetch(&tmB);
     for (int s = 0; s < 2; ++s) {
       tc::mbar_init(&full[s], 1);
+      tc::mbar_init(&conv[s], CONV_WARPS);
       tc::mbar_init(&empty[s], 1);
       tc::mbar_init(&tfull[s], 1);
       tc::mbar_init(&tempty[s], EPI_WARPS);
@@ -90,7 +96,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     for (long long t = blockIdx.x; t < args.n_tiles; t += gridDim.x, ++j) {
       const int s = j & 1;
       tc::mbar_wait(&empty[s], ((j >> 1) & 1) ^ 1);
-      tc::mbar_expect_tx(&full[s], stage_bytes);
+      tc::mbar_expect_tx(&full[s], tma_bytes);
       const int r0 = (int)((t % args.n_rb) * 128), c0 = (int)((t / args.n_rb) * N);
       uint8_t* a = smem + s * stage_bytes;
       uint8_t* b = a + a_bytes;
@@ -108,20 +114,37 @@ __global__ void __launch_bounds__(THREADS, 1)
       const int s = j & 1;
       const uint32_t ph = (j >> 1) & 1;
       tc::mbar_wait(&tempty[s], ph ^ 1);
-      tc::mbar_wait(&full[s], ph);
+      tc::mbar_wait(&conv[s], ph);
       tc::fence_after_sync();
       const uint32_t a = tc::smem_u32(smem + s * stage_bytes);
       const uint32_t b = a + a_bytes;
       for (int kk = 0; kk < kp / 8; ++kk) {
         const uint64_t ad = tc::sdesc(a + kk * 1024, chunk, 512, 1);
         const uint64_t bd = tc::sdesc(b + kk * 1024, chunk, 512, 1);
-        tc::mma_tf32(tmem + s * N, ad, bd, idesc, kk != 0);
+        if (SPLIT) {
+          tc::mma_tf32(tmem + s * N, tc::sdesc(a + tma_bytes + kk * 1024, chunk, 512, 1), bd, idesc, kk != 0);
+          tc::mma_tf32(tmem + s * N, ad, tc::sdesc(b + tma_bytes + kk * 1024, chunk, 512, 1), idesc, 1);
+        }
+        tc::mma_tf32(tmem + s * N, ad, bd, idesc, SPLIT || kk != 0);
       }
       tc::mma_commit(&empty[s]);
       tc::mma_commit(&tfull[s]);
     }
-  } else if (warp >= 2) {
-    const int ew = warp - 2;
+  } else if (warp >= 2 && warp < EPI0) {
+    // operand rounding (TF32 round-to-nearest) or 3xTF32 hi/lo split
+    const int ct = threadIdx.x - 64;
+    int j = 0;
+    for (long long t = blockIdx.x; t < args.n_tiles; t += gridDim.x, ++j) {
+      const int s = j & 1;
+      tc::mbar_wait(&full[s], (j >> 1) & 1);
+      uint8_t* a = smem + s * stage_bytes;
+      tc::tf32_split_tile<SPLIT>(a, a + tma_bytes, (int)(tma_bytes / 4), ct, 32 * CONV_WARPS);
+      tc::fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&conv[s]);
+    }
+  } else if (warp >= EPI0) {
+    const int ew = warp - EPI0;
     const int quad = warp & 3;
     const int half = ew >> 2;  // column half handled by this warp
     const int row = 32 * quad + lane;
@@ -200,16 +223,21 @@ __global__ void __launch_bounds__(THREADS, 1)
   }
 }
 
-template <int N>
-int go(const CUtensorMap& ma, const CUtensorMap& mb, const ComposeArgs& a, int grid, cudaStream_t st) {
-  const int smem = 2 * (128 + N) * a.kp * 4 + 1024 + 256;
-  auto fn = k_compose_tc<N>;
+template <int N, bool SPLIT>
+int go2(const CUtensorMap& ma, const CUtensorMap& mb, const ComposeArgs& a, int grid, cudaStream_t st) {
+  const int smem = 2 * (128 + N) * a.kp * 4 * (SPLIT ? 2 : 1) + 1024 + 256;
+  auto fn = k_compose_tc<N, SPLIT>;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) throw std::runtime_error(std::string("compose_tc smem: ") + cudaGetErrorString(e));
   fn<<<grid, THREADS, smem, st>>>(ma, mb, a);
   e = cudaGetLastError();
   if (e != cudaSuccess) throw std::runtime_error(std::string("compose_tc: ") + cudaGetErrorString(e));
   return grid;
+}
+
+template <int N>
+int go(const CUtensorMap& ma, const CUtensorMap& mb, const ComposeArgs& a, int grid, bool split3, cudaStream_t st) {
+  return split3 ? go2<N, true>(ma, mb, a, grid, st) : go2<N, false>(ma, mb, a, grid, st);
 }
 
 }  // namespace
@@ -224,7 +252,7 @@ bool tc_compose_supported(int64_t I, int64_t P, int64_t p, int64_t S) {
 
 int launch_compose_tc(const float* A, const float* M, const float* Xo, const uint32_t* maskbits, float* Xn,
                       int64_t I, int64_t P, int64_t S, int64_t p, double rho, bool objective_only, double* partials,
-                      int64_t partial_cap, int n_sm, cudaStream_t st) {
+                      int64_t partial_cap, int n_sm, bool split3, cudaStream_t st) {
   ComposeArgs a;
   a.Xo = Xo;
   a.Xn = Xn;
@@ -245,7 +273,7 @@ int launch_compose_tc(const float* A, const float* M, const float* Xo, const uin
     N = (int)((I + 31) / 32 * 32);
     if (N > 256) N = 256;
   }
-  while (N > 32 && 2 * (128 + N) * a.kp * 4 + 1280 > 200 * 1024) N /= 2;
+  while (N > 32 && 2 * (128 + N) * a.kp * 4 * (split3 ? 2 : 1) + 1280 > 200 * 1024) N /= 2;
   if (N != 32 && N != 64 && N != 96 && N != 128 && N != 160 && N != 192 && N != 224 && N != 256) N = 256;
   a.n_rb = (a.rows + 127) / 128;
   const long long n_cb = (a.cols + N - 1) / N;
@@ -261,14 +289,14 @@ int launch_compose_tc(const float* A, const float* M, const float* Xo, const uin
   const CUtensorMap& rowsmap = a.rows_are_p ? mM : mA;
   const CUtensorMap& colsmap = a.rows_are_p ? mA : mM;
   switch (N) {
-    case 32: return go<32>(rowsmap, colsmap, a, grid, st);
-    case 64: return go<64>(rowsmap, colsmap, a, grid, st);
-    case 96: return go<96>(rowsmap, colsmap, a, grid, st);
-    case 128: return go<128>(rowsmap, colsmap, a, grid, st);
-    case 160: return go<160>(rowsmap, colsmap, a, grid, st);
-    case 192: return go<192>(rowsmap, colsmap, a, grid, st);
-    case 224: return go<224>(rowsmap, colsmap, a, grid, st);
-    default: return go<256>(rowsmap, colsmap, a, grid, st);
+    case 32: return go<32>(rowsmap, colsmap, a, grid, split3, st);
+    case 64: return go<64>(rowsmap, colsmap, a, grid, split3, st);
+    case 96: return go<96>(rowsmap, colsmap, a, grid, split3, st);
+    case 128: return go<128>(rowsmap, colsmap, a, grid, split3, st);
+    case 160: return go<160>(rowsmap, colsmap, a, grid, split3, st);
+    case 192: return go<192>(rowsmap, colsmap, a, grid, split3, st);
+    case 224: return go<224>(rowsmap, colsmap, a, grid, split3, st);
+    default: return go<256>(rowsmap, colsmap, a, grid, split3, st);
   }
 }
 

@@ -367,7 +367,8 @@ class Ctx : public Executor {
 
   int target_ctas() const { return n_sm * 4; }
   int n_sm = 148;
-  bool use_tc = true;  // fp32 K2 on tcgen05 (FCTN_NO_TC=1 forces the SIMT path)
+  bool use_tc = true;  // fp32 K2/K4 on tcgen05 (FCTN_NO_TC=1 forces the SIMT path)
+  bool split3 = true;  // 3xTF32 products (FCTN_TF32=1x: one round-to-nearest TF32 pass)
   bool tc_ok(int k) const {
     if (dtype != FCTN_F32 || !use_tc) return false;
     int64_t P = 1, Q = 1;
@@ -394,7 +395,7 @@ class Ctx : public Executor {
       if (tc_ok(k)) {
         int64_t P = 1;
         for (int j = 0; j < k; ++j) P *= sh.dims[j];
-        TcStreamPlan tp = plan_stream_tc(I, P, p / P, S, n_sm);
+        TcStreamPlan tp = plan_stream_tc(I, P, p / P, S, n_sm, split3);
         max_yp = std::max(max_yp, (tp.nsplit * I * S + 1) / 2);  // float partials in the double buffer
       }
       max_part = std::max(max_part, ((I + 63) / 64) * ((p + 63) / 64));
@@ -546,6 +547,8 @@ class Ctx : public Executor {
     {
       const char* e = getenv("FCTN_NO_TC");
       use_tc = !(e && e[0] == '1');
+      const char* t = getenv("FCTN_TF32");
+      split3 = !(t && std::string(t) == "1x");
     }
     CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
     CK(cudaEventCreate(&ev0));
@@ -612,7 +615,7 @@ class Ctx : public Executor {
     int nsplit = 0;
     const bool tc = tc_ok(k);
     if (tc) {
-      TcStreamPlan tp = plan_stream_tc(I, P, p / P, S, n_sm);
+      TcStreamPlan tp = plan_stream_tc(I, P, p / P, S, n_sm, split3);
       launch_stream_tc((const float*)X[cur], (const float*)Mbuf, (float*)ypart, I, P, p / P, S, tp, st);
       nsplit = (int)tp.nsplit;
     } else {
@@ -666,7 +669,7 @@ class Ctx : public Executor {
     int pm = pbegin(FCTN_K_COMPOSE);
     if (dtype == FCTN_F32 && use_tc && tc_compose_supported(I, P, p, S))
       nb = launch_compose_tc((const float*)Ac[k], (const float*)Mbuf, (const float*)X[cur], maskbits,
-                             (float*)X[cur ^ 1], I, P, S, p, rho, objective_only, partials, partial_cap, n_sm, st);
+                             (float*)X[cur ^ 1], I, P, S, p, rho, objective_only, partials, partial_cap, n_sm, split3, st);
     else if (dtype == FCTN_F64)
       nb = launch_compose<double>((const double*)Ac[k], (const double*)Mbuf, (const double*)X[cur], mask,
                                   (double*)X[cur ^ 1], I, P, S, p, rho, objective_only, partials, partial_cap, st);
@@ -1009,7 +1012,7 @@ int fctn_selftest_stream(int device, int dtype, int use_tc, int64_t I, int64_t P
     CK(cudaMemcpy(dx, x, T * es, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(dm, m, p * S * es, cudaMemcpyHostToDevice));
     if (use_tc && dtype == FCTN_F32 && fctn::tc_stream_supported(I, P, Q, S)) {
-      fctn::TcStreamPlan tp = fctn::plan_stream_tc(I, P, Q, S, nsm);
+      fctn::TcStreamPlan tp = fctn::plan_stream_tc(I, P, Q, S, nsm, !(getenv("FCTN_TF32") && std::string(getenv("FCTN_TF32")) == "1x"));
       CK(cudaMalloc(&part, tp.nsplit * I * S * sizeof(float)));
       fctn::launch_stream_tc((const float*)dx, (const float*)dm, (float*)part, I, P, Q, S, tp, st);
       fctn::launch_reduce_splits_f32((const float*)part, (int)tp.nsplit, I * S, nullptr, 0.0, dy, st);

@@ -57,9 +57,10 @@ struct TcStreamPlan {
   int64_t nkb;         // K blocks in total
   int64_t kb_per_split;
   int64_t nsplit;
+  bool split3;         // 3xTF32 (hi/lo split) instead of round-to-nearest TF32
 };
 bool tc_stream_supported(int64_t I, int64_t P, int64_t Q, int64_t S);
-TcStreamPlan plan_stream_tc(int64_t I, int64_t P, int64_t Q, int64_t S, int n_sm);
+TcStreamPlan plan_stream_tc(int64_t I, int64_t P, int64_t Q, int64_t S, int n_sm, bool split3);
 void launch_stream_tc(const float* X, const float* M, float* part, int64_t I, int64_t P, int64_t Q, int64_t S,
                       const TcStreamPlan& tp, cudaStream_t st);
 
@@ -103,7 +104,7 @@ int launch_compose(const T* A, const T* M, const T* Xold, const uint8_t* mask, T
 bool tc_compose_supported(int64_t I, int64_t P, int64_t p, int64_t S);
 int launch_compose_tc(const float* A, const float* M, const float* Xo, const uint32_t* maskbits, float* Xn,
                       int64_t I, int64_t P, int64_t S, int64_t p, double rho, bool objective_only, double* partials,
-                      int64_t partial_cap, int n_sm, cudaStream_t st);
+                      int64_t partial_cap, int n_sm, bool split3, cudaStream_t st);
 void launch_pack_mask(const uint8_t* mask, int64_t T, uint32_t* bits, cudaStream_t st);
 // fixed-order final reduction of n x 4 partials into out[0..3]
 void launch_reduce4(const double* partials, int64_t n, double* out, cudaStream_t st);

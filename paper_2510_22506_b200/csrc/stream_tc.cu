@@ -4,8 +4,11 @@
 // One CTA = one 128-row tile of mode k x one split of the reduction axis p.
 // Warp roles (192 threads):
 //   warp 0      TMA producer: X tile (128 x 32 fp32) + M tile (NT x 32) per stage
-//   warp 1      TMEM allocator + single-thread MMA issuer (4 x K=8 per stage)
-//   warps 2..5  epilogue: tcgen05.ld the 128 x NT accumulator, write fp32 partials
+//   warp 1      TMEM allocator + single-thread MMA issuer (4 x K=8 per stage,
+//               x3 for the 3xTF32 split)
+//   warps 2..5  per stage: round the landed tiles to TF32 (round-to-nearest)
+//               or split them hi/lo for 3xTF32 (tc_common.cuh); at the end:
+//               tcgen05.ld the 128 x NT accumulator, write fp32 partials
 // X is read in place through a TMA descriptor of the mode-k view:
 //   P > 1  (modes before k exist): 3-D [P, I, Q], K-major A tile (rows = i,
 //          128 B = 32 consecutive p along the fastest mode)
@@ -31,26 +34,29 @@ namespace fctn {
 namespace {
 
 constexpr int BK = 32;  // fp32 per 128-byte row
-constexpr int STAGES = 6;
 constexpr int A_BYTES = 128 * BK * 4;  // 16 KB
 
-template <int NT>
+// stage = [A hi | B hi | (A lo | B lo)]; TMA bytes = A + B
+template <int NT, bool SPLIT>
 struct StreamSmem {
   static constexpr int B_BYTES = NT * BK * 4;
-  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int TMA_BYTES = A_BYTES + B_BYTES;
+  static constexpr int STAGE_BYTES = TMA_BYTES * (SPLIT ? 2 : 1);
+  static constexpr int STAGES = (200 * 1024) / STAGE_BYTES > 6 ? 6 : (200 * 1024) / STAGE_BYTES;
   static constexpr int TOTAL = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
 };
 
-template <int NT, bool AMN>
+template <int NT, bool AMN, bool SPLIT>
 __global__ void __launch_bounds__(192, 1)
     k_stream_tc(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmM,
                 float* __restrict__ part, int I, int S, long long nkb_total, long long kb_per_split, int nPB) {
+  using L = StreamSmem<NT, SPLIT>;
+  constexpr int STAGES = L::STAGES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sA = smem;
-  uint8_t* sB = smem + STAGES * A_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * StreamSmem<NT>::STAGE_BYTES);
-  uint64_t* empty = full + STAGES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * L::STAGE_BYTES);
+  uint64_t* conv = full + STAGES;
+  uint64_t* empty = conv + STAGES;
   uint64_t* tmem_full = empty + STAGES;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
 
@@ -68,6 +74,7 @@ __global__ void __launch_bounds__(192, 1)
     tc::tma_prefetch(&tmM);
     for (int s = 0; s < STAGES; ++s) {
       tc::mbar_init(&full[s], 1);
+      tc::mbar_init(&conv[s], 4);
       tc::mbar_init(&empty[s], 1);
     }
     tc::mbar_init(tmem_full, 1);
@@ -86,10 +93,10 @@ __global__ void __launch_bounds__(192, 1)
       const int s = it % STAGES;
       const uint32_t ph = (it / STAGES) & 1;
       tc::mbar_wait(&empty[s], ph ^ 1);
-      tc::mbar_expect_tx(&full[s], StreamSmem<NT>::STAGE_BYTES);
+      tc::mbar_expect_tx(&full[s], L::TMA_BYTES);
       const long long kb = kb0 + it;
-      uint8_t* a = sA + s * A_BYTES;
-      uint8_t* b = sB + s * StreamSmem<NT>::B_BYTES;
+      uint8_t* a = smem + s * L::STAGE_BYTES;
+      uint8_t* b = a + A_BYTES;
       if (AMN) {
         const int q0 = (int)(kb * BK);
 #pragma unroll
@@ -108,21 +115,38 @@ __global__ void __launch_bounds__(192, 1)
     for (int it = 0; it < nkb; ++it) {
       const int s = it % STAGES;
       const uint32_t ph = (it / STAGES) & 1;
-      tc::mbar_wait(&full[s], ph);
+      tc::mbar_wait(&conv[s], ph);
       tc::fence_after_sync();
-      const uint32_t a = tc::smem_u32(sA + s * A_BYTES);
-      const uint32_t b = tc::smem_u32(sB + s * StreamSmem<NT>::B_BYTES);
+      const uint32_t a = tc::smem_u32(smem + s * L::STAGE_BYTES);
+      const uint32_t b = a + A_BYTES;
+      const uint32_t lo = L::TMA_BYTES;  // lo tiles follow the hi tiles
 #pragma unroll
       for (int kk = 0; kk < BK / 8; ++kk) {
         const uint64_t ad = AMN ? tc::sdesc(a + kk * 1024, 4096, 512, 1) : tc::sdesc(a + kk * 32, 16, 1024);
         const uint64_t bd = tc::sdesc(b + kk * 32, 16, 1024);
-        tc::mma_tf32(tmem, ad, bd, idesc, (it | kk) != 0);
+        if (SPLIT) {
+          const uint64_t adl = AMN ? tc::sdesc(a + lo + kk * 1024, 4096, 512, 1) : tc::sdesc(a + lo + kk * 32, 16, 1024);
+          const uint64_t bdl = tc::sdesc(b + lo + kk * 32, 16, 1024);
+          tc::mma_tf32(tmem, adl, bd, idesc, (it | kk) != 0);
+          tc::mma_tf32(tmem, ad, bdl, idesc, 1);
+        }
+        tc::mma_tf32(tmem, ad, bd, idesc, SPLIT || (it | kk) != 0);
       }
       tc::mma_commit(&empty[s]);
     }
     tc::mma_commit(tmem_full);
   } else if (warp >= 2) {
-    // ---------------- epilogue
+    // ---------------- operand rounding / 3xTF32 split, then the epilogue
+    const int ct = threadIdx.x - 64;
+    for (int it = 0; it < nkb; ++it) {
+      const int s = it % STAGES;
+      tc::mbar_wait(&full[s], (it / STAGES) & 1);
+      uint8_t* a = smem + s * L::STAGE_BYTES;
+      tc::tf32_split_tile<SPLIT>(a, a + L::TMA_BYTES, L::TMA_BYTES / 4, ct, 128);
+      tc::fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&conv[s]);
+    }
     tc::mbar_wait(tmem_full, 0);
     tc::fence_after_sync();
     const int q = warp & 3;
@@ -175,17 +199,26 @@ CUtensorMap make_map(const void* base, int rank, const uint64_t* dims, const uin
   return m;
 }
 
-template <int NT, bool AMN>
-void go(const CUtensorMap& mx, const CUtensorMap& mm, float* part, int64_t I, int64_t S, const TcStreamPlan& tp,
-        cudaStream_t st) {
-  const int smem = StreamSmem<NT>::TOTAL;
-  auto fn = k_stream_tc<NT, AMN>;
+template <int NT, bool AMN, bool SPLIT>
+void go3(const CUtensorMap& mx, const CUtensorMap& mm, float* part, int64_t I, int64_t S, const TcStreamPlan& tp,
+         cudaStream_t st) {
+  const int smem = StreamSmem<NT, SPLIT>::TOTAL;
+  auto fn = k_stream_tc<NT, AMN, SPLIT>;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) throw std::runtime_error(std::string("stream_tc smem: ") + cudaGetErrorString(e));
   dim3 grid((unsigned)tp.n_mtiles, (unsigned)tp.nsplit);
   fn<<<grid, 192, smem, st>>>(mx, mm, part, (int)I, (int)S, tp.nkb, tp.kb_per_split, (int)tp.npb);
   e = cudaGetLastError();
   if (e != cudaSuccess) throw std::runtime_error(std::string("stream_tc: ") + cudaGetErrorString(e));
+}
+
+template <int NT, bool AMN>
+void go(const CUtensorMap& mx, const CUtensorMap& mm, float* part, int64_t I, int64_t S, const TcStreamPlan& tp,
+        cudaStream_t st) {
+  if (tp.split3)
+    go3<NT, AMN, true>(mx, mm, part, I, S, tp, st);
+  else
+    go3<NT, AMN, false>(mx, mm, part, I, S, tp, st);
 }
 
 }  // namespace
@@ -203,8 +236,9 @@ bool tc_stream_supported(int64_t I, int64_t P, int64_t Q, int64_t S) {
   return P % 4 == 0;
 }
 
-TcStreamPlan plan_stream_tc(int64_t I, int64_t P, int64_t Q, int64_t S, int n_sm) {
+TcStreamPlan plan_stream_tc(int64_t I, int64_t P, int64_t Q, int64_t S, int n_sm, bool split3) {
   TcStreamPlan tp;
+  tp.split3 = split3;
   tp.nt = S <= 32 ? 32 : S <= 64 ? 64 : S <= 96 ? 96 : 128;
   tp.n_mtiles = (I + 127) / 128;
   tp.npb = P == 1 ? 1 : (P + BK - 1) / BK;

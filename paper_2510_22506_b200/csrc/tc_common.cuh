@@ -108,6 +108,38 @@ __device__ __forceinline__ void fence_before_sync() {
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
 }
 
+// generic-proxy smem writes -> visible to the async proxy (UMMA operand reads)
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+// ------------------------------------------------------------------ TF32 operand split
+// The tensor core reads fp32 operands as TF32 by dropping the low 13 mantissa
+// bits (a biased truncation).  Tiles are rewritten in shared memory as
+// hi = rn_tf32(x) (round to nearest) and, for the 3xTF32 product
+// D = Ah Bh + Al Bh + Ah Bl, lo = x - hi (exact in fp32; its own truncation
+// costs ~2^-22 relative), giving FP32-class products at 3x the MMA work.
+__device__ __forceinline__ float tf32_rn(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+template <bool SPLIT>
+__device__ __forceinline__ void tf32_split_tile(uint8_t* hi, uint8_t* lo, int nfloat, int tid, int nthr) {
+  float4* h4 = reinterpret_cast<float4*>(hi);
+  float4* l4 = reinterpret_cast<float4*>(lo);
+  for (int e = tid; e < nfloat / 4; e += nthr) {
+    const float4 v = h4[e];
+    float4 h;
+    h.x = tf32_rn(v.x);
+    h.y = tf32_rn(v.y);
+    h.z = tf32_rn(v.z);
+    h.w = tf32_rn(v.w);
+    h4[e] = h;
+    if (SPLIT) l4[e] = make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w);
+  }
+}
+
 // ------------------------------------------------------------------ TMEM
 template <int NCOLS>
 __device__ __forceinline__ void tmem_alloc(uint32_t* dst_smem) {
