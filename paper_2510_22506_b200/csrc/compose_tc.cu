@@ -7,12 +7,14 @@
 //   P > 1  (k > 0): rows = p (M_k columns), cols = i (mode-k rows)
 //   P == 1 (k = 0): rows = i, cols = p
 // Both operands are MN-major 32-bit tiles (SWIZZLE_128B_BASE32B, TMA 32-B
-// atoms) with K = s.  Persistent CTAs (one per SM) walk the tiles with a
-// 2-stage smem ring and a double-buffered TMEM accumulator, so the MMA of
-// tile t+1 overlaps the epilogue of tile t.
-// Warp roles (448 threads): warp 0 TMA, warp 1 TMEM alloc + MMA issue,
-// warps 2..5 TF32 rounding / 3xTF32 split of the landed operand tiles,
-// warps 6..13 epilogue (two warps per TMEM lane quadrant, column halves).
+// atoms) with K = s.  Persistent CTAs (one per SM) walk the tiles with one
+// operand stage and a double-buffered TMEM accumulator, so the MMA of tile
+// t+1 overlaps the epilogue of tile t; the producer also bulk-prefetches each
+// tile's X_old rows into L2 so the epilogue's loads hit L2.
+// Warp roles (704 threads): warp 0 TMA + L2 prefetch, warp 1 TMEM alloc +
+// MMA issue, warps 2..5 TF32 rounding / 3xTF32 split of the landed operand
+// tiles, warps 6..21 epilogue (four warps per TMEM lane quadrant, column
+// quarters).
 // The observation mask is read bit-packed (1 bit per entry, F order).
 #include <cuda.h>
 #include <cudaTypedefs.h>
@@ -33,9 +35,10 @@ CUtensorMap tc_make_map_f32(const void* base, int rank, const uint64_t* dims, co
 namespace {
 
 constexpr int CONV_WARPS = 4;
-constexpr int EPI_WARPS = 8;
+constexpr int EPI_WARPS = 16;
 constexpr int EPI0 = 2 + CONV_WARPS;  // first epilogue warp
-constexpr int THREADS = 32 * (EPI0 + EPI_WARPS);
+constexpr int NWARPS = EPI0 + EPI_WARPS;
+constexpr int THREADS = 32 * NWARPS;
 
 struct ComposeArgs {
   const float* Xo;
@@ -47,9 +50,21 @@ struct ComposeArgs {
   long long P, PI, I;         // X view
   int kp;                     // K (= s padded to 8)
   int rows_are_p;
+  int prefetch;               // rows of a tile are contiguous in X: bulk-prefetch them to L2
   float rho, onep;
   int objective_only;
 };
+
+__device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(reinterpret_cast<uint64_t>(p)), "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
 
 template <int N, bool SPLIT>
 __global__ void __launch_bounds__(THREADS, 1)
@@ -61,13 +76,13 @@ __global__ void __launch_bounds__(THREADS, 1)
   const uint32_t a_bytes = 128u * kp * 4u, b_bytes = (uint32_t)N * kp * 4u;
   const uint32_t tma_bytes = a_bytes + b_bytes;
   const uint32_t stage_bytes = tma_bytes * (SPLIT ? 2 : 1);  // [A hi | B hi | (A lo | B lo)]
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + 2 * stage_bytes);
-  uint64_t* conv = full + 2;
-  uint64_t* empty = conv + 2;
-  uint64_t* tfull = empty + 2;
-  uint64_t* tempty = tfull + 2;  // (barrier block: 10 x 8 B)
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + stage_bytes);
+  uint64_t* conv = full + 1;
+  uint64_t* empty = conv + 1;
+  uint64_t* tfull = empty + 1;   // [2]
+  uint64_t* tempty = tfull + 2;  // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-  __shared__ double red[4][THREADS];
+  __shared__ double red[4][NWARPS];
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   constexpr int NCOLS = 2 * N <= 32 ? 32 : 2 * N <= 64 ? 64 : 2 * N <= 128 ? 128 : 2 * N <= 256 ? 256 : 512;
@@ -75,10 +90,10 @@ __global__ void __launch_bounds__(THREADS, 1)
   if (warp == 0 && lane == 0) {
     tc::tma_prefetch(&tmA);
     tc::tma_prefetch(&tmB);
+    tc::mbar_init(full, 1);
+    tc::mbar_init(conv, CONV_WARPS);
+    tc::mbar_init(empty, 1);
     for (int s = 0; s < 2; ++s) {
-      tc::mbar_init(&full[s], 1);
-      tc::mbar_init(&conv[s], CONV_WARPS);
-      tc::mbar_init(&empty[s], 1);
       tc::mbar_init(&tfull[s], 1);
       tc::mbar_init(&tempty[s], EPI_WARPS);
     }
@@ -92,31 +107,46 @@ __global__ void __launch_bounds__(THREADS, 1)
   double s_d = 0.0, s_b = 0.0, s_c = 0.0, s_n = 0.0;
 
   if (warp == 0 && lane == 0) {
+    // ---- TMA producer (one operand stage: the K = s MMA is short, the TMEM
+    // double buffer is what overlaps tile t+1's MMA with tile t's epilogue)
     int j = 0;
     for (long long t = blockIdx.x; t < args.n_tiles; t += gridDim.x, ++j) {
-      const int s = j & 1;
-      tc::mbar_wait(&empty[s], ((j >> 1) & 1) ^ 1);
-      tc::mbar_expect_tx(&full[s], tma_bytes);
-      const int r0 = (int)((t % args.n_rb) * 128), c0 = (int)((t / args.n_rb) * N);
-      uint8_t* a = smem + s * stage_bytes;
+      tc::mbar_wait(empty, (j & 1) ^ 1);
+      tc::mbar_expect_tx(full, tma_bytes);
+      const long long rb = t % args.n_rb, cb = t / args.n_rb;
+      const int r0 = (int)(rb * 128), c0 = (int)(cb * N);
+      uint8_t* a = smem;
       uint8_t* b = a + a_bytes;
       const uint32_t chunk = 32u * kp * 4u;
 #pragma unroll
-      for (int c = 0; c < 4; ++c) tc::tma_load_2d(a + c * chunk, &tmA, &full[s], r0 + 32 * c, 0);
+      for (int c = 0; c < 4; ++c) tc::tma_load_2d(a + c * chunk, &tmA, full, r0 + 32 * c, 0);
 #pragma unroll
-      for (int c = 0; c < N / 32; ++c) tc::tma_load_2d(b + c * chunk, &tmB, &full[s], c0 + 32 * c, 0);
+      for (int c = 0; c < N / 32; ++c) tc::tma_load_2d(b + c * chunk, &tmB, full, c0 + 32 * c, 0);
+      if (args.prefetch) {
+        // stream this tile's X_old rows (and mask words) into L2 ahead of the epilogue
+        const long long rbase = args.rows_are_p ? (r0 % args.P) + args.PI * (r0 / args.P) : r0;
+        const long long cstride = args.rows_are_p ? args.P : args.I;
+        const long long nrow = args.rows - r0 < 128 ? args.rows - r0 : 128;
+        for (int c = 0; c < N; ++c) {
+          const long long gc = c0 + c;
+          if (gc >= args.cols) break;
+          const long long off = rbase + cstride * gc;
+          prefetch_l2(args.Xo + off, (uint32_t)(((nrow * 4) + 15) & ~15LL));
+          if (!args.objective_only) prefetch_l2(args.maskbits + (off >> 5), 16);
+        }
+      }
     }
   } else if (warp == 1 && lane == 0) {
+    // ---- MMA issuer
     constexpr uint32_t idesc = tc::idesc_tf32(128, N, true, true);
     const uint32_t chunk = 32u * kp * 4u;
     int j = 0;
     for (long long t = blockIdx.x; t < args.n_tiles; t += gridDim.x, ++j) {
       const int s = j & 1;
-      const uint32_t ph = (j >> 1) & 1;
-      tc::mbar_wait(&tempty[s], ph ^ 1);
-      tc::mbar_wait(&conv[s], ph);
+      tc::mbar_wait(&tempty[s], ((j >> 1) & 1) ^ 1);
+      tc::mbar_wait(conv, j & 1);
       tc::fence_after_sync();
-      const uint32_t a = tc::smem_u32(smem + s * stage_bytes);
+      const uint32_t a = tc::smem_u32(smem);
       const uint32_t b = a + a_bytes;
       for (int kk = 0; kk < kp / 8; ++kk) {
         const uint64_t ad = tc::sdesc(a + kk * 1024, chunk, 512, 1);
@@ -127,26 +157,26 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
         tc::mma_tf32(tmem + s * N, ad, bd, idesc, SPLIT || kk != 0);
       }
-      tc::mma_commit(&empty[s]);
+      tc::mma_commit(empty);
       tc::mma_commit(&tfull[s]);
     }
   } else if (warp >= 2 && warp < EPI0) {
-    // operand rounding (TF32 round-to-nearest) or 3xTF32 hi/lo split
+    // ---- operand rounding (TF32 round-to-nearest) or 3xTF32 hi/lo split
     const int ct = threadIdx.x - 64;
     int j = 0;
     for (long long t = blockIdx.x; t < args.n_tiles; t += gridDim.x, ++j) {
-      const int s = j & 1;
-      tc::mbar_wait(&full[s], (j >> 1) & 1);
-      uint8_t* a = smem + s * stage_bytes;
-      tc::tf32_split_tile<SPLIT>(a, a + tma_bytes, (int)(tma_bytes / 4), ct, 32 * CONV_WARPS);
+      tc::mbar_wait(full, j & 1);
+      tc::tf32_split_tile<SPLIT>(smem, smem + tma_bytes, (int)(tma_bytes / 4), ct, 32 * CONV_WARPS);
       tc::fence_proxy_async_smem();
       __syncwarp();
-      if (lane == 0) tc::mbar_arrive(&conv[s]);
+      if (lane == 0) tc::mbar_arrive(conv);
     }
   } else if (warp >= EPI0) {
+    // ---- epilogue: TMEM -> registers, blend with X_old, write X_new, reduce
     const int ew = warp - EPI0;
     const int quad = warp & 3;
-    const int half = ew >> 2;  // column half handled by this warp
+    const int part = ew >> 2;                  // column quarter of this warp
+    constexpr int CW = N / 4;                  // columns per warp (multiple of 8)
     const int row = 32 * quad + lane;
     int j = 0;
     for (long long t = blockIdx.x; t < args.n_tiles; t += gridDim.x, ++j) {
@@ -154,50 +184,55 @@ __global__ void __launch_bounds__(THREADS, 1)
       tc::mbar_wait(&tfull[s], (j >> 1) & 1);
       tc::fence_after_sync();
       const long long gr = (t % args.n_rb) * 128 + row;
-      const long long cb = (t / args.n_rb) * N;
+      const long long cb = (t / args.n_rb) * N + part * CW;
       const bool row_ok = gr < args.rows;
-      long long rowbase, colstride;
-      if (args.rows_are_p) {
-        rowbase = (gr % args.P) + args.PI * (gr / args.P);
-        colstride = args.P;
-      } else {
-        rowbase = gr;
-        colstride = args.I;
-      }
+      const long long rowbase = args.rows_are_p ? (gr % args.P) + args.PI * (gr / args.P) : gr;
+      const long long colstride = args.rows_are_p ? args.P : args.I;
+      const uint32_t taddr = tmem + s * N + ((uint32_t)(32 * quad) << 16) + part * CW;
 #pragma unroll 1
-      for (int c0 = half * (N / 2); c0 < (half + 1) * (N / 2); c0 += 16) {
-        float v[16];
-        tc::tmem_ld16(tmem + s * N + ((uint32_t)(32 * quad) << 16) + c0, v);
-        if (row_ok) {
+      for (int c0 = 0; c0 < CW; c0 += 8) {
+        uint32_t r[8];
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                     : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+                       "=r"(r[7])
+                     : "r"(taddr + c0));
+        float x[8];
+        uint32_t mw[8];
+        long long off0 = rowbase + colstride * (cb + c0);
+        const long long rem = args.cols - (cb + c0);
+        const int nc = rem < 8 ? (int)rem : 8;
 #pragma unroll
-          for (int q = 0; q < 16; ++q) {
-            const long long gc = cb + c0 + q;
-            if (gc < args.cols) {
-              const long long off = rowbase + colstride * gc;
-              const float x = __ldcs(args.Xo + off);
-              const float c = v[q];
-              if (args.objective_only) {
-                const double d = (double)x - (double)c;
-                s_c += d * d;
-              } else {
-                const bool obs = (__ldg(args.maskbits + (off >> 5)) >> (off & 31)) & 1u;
-                float xn;
-                if (obs) {
-                  xn = x;  // observed entries restored bit for bit (solver.py:235-236)
-                } else {
-                  float tt = x * args.rho;  // (x*rho + c)/(1+rho), solver.py:232-234
-                  tt = tt + c;
-                  xn = tt / args.onep;
-                }
-                __stcs(args.Xn + off, xn);
-                const double dx = (double)xn - (double)x;
-                const double dc = (double)xn - (double)c;
-                s_d += dx * dx;
-                s_b += (double)x * (double)x;
-                s_c += dc * dc;
-                s_n += (double)xn * (double)xn;
-              }
+        for (int q = 0; q < 8; ++q) {  // all loads in flight before the TMEM wait
+          const long long off = off0 + colstride * q;
+          x[q] = (row_ok && q < nc) ? __ldcs(args.Xo + off) : 0.0f;
+          mw[q] = (row_ok && q < nc && !args.objective_only) ? __ldg(args.maskbits + (off >> 5)) : 0u;
+        }
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        if (!row_ok) continue;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          if (q >= nc) break;
+          const long long off = off0 + colstride * q;
+          const float c = __uint_as_float(r[q]);
+          if (args.objective_only) {
+            const double d = (double)x[q] - (double)c;
+            s_c += d * d;
+          } else {
+            float xn;
+            if ((mw[q] >> (off & 31)) & 1u) {
+              xn = x[q];  // observed entries restored bit for bit (solver.py:235-236)
+            } else {
+              float tt = x[q] * args.rho;  // (x*rho + c)/(1+rho), solver.py:232-234
+              tt = tt + c;
+              xn = tt / args.onep;
             }
+            __stcs(args.Xn + off, xn);
+            const double dx = (double)xn - (double)x[q];
+            const double dc = (double)xn - (double)c;
+            s_d += dx * dx;
+            s_b += (double)x[q] * (double)x[q];
+            s_c += dc * dc;
+            s_n += (double)xn * (double)xn;
           }
         }
       }
@@ -206,15 +241,22 @@ __global__ void __launch_bounds__(THREADS, 1)
       if (lane == 0) tc::mbar_arrive(&tempty[s]);
     }
   }
-  red[0][threadIdx.x] = s_d;
-  red[1][threadIdx.x] = s_b;
-  red[2][threadIdx.x] = s_c;
-  red[3][threadIdx.x] = s_n;
+  // fixed-order reduction: warp shuffle tree, then warps in index order
+  s_d = warp_sum(s_d);
+  s_b = warp_sum(s_b);
+  s_c = warp_sum(s_c);
+  s_n = warp_sum(s_n);
+  if (lane == 0) {
+    red[0][warp] = s_d;
+    red[1][warp] = s_b;
+    red[2][warp] = s_c;
+    red[3][warp] = s_n;
+  }
   tc::fence_before_sync();
   __syncthreads();
   if (threadIdx.x < 4) {
     double v = 0.0;
-    for (int q = 0; q < THREADS; ++q) v += red[threadIdx.x][q];  // fixed order
+    for (int q = 0; q < NWARPS; ++q) v += red[threadIdx.x][q];
     args.partials[blockIdx.x * 4 + threadIdx.x] = v;
   }
   if (warp == 1) {
@@ -225,7 +267,7 @@ __global__ void __launch_bounds__(THREADS, 1)
 
 template <int N, bool SPLIT>
 int go2(const CUtensorMap& ma, const CUtensorMap& mb, const ComposeArgs& a, int grid, cudaStream_t st) {
-  const int smem = 2 * (128 + N) * a.kp * 4 * (SPLIT ? 2 : 1) + 1024 + 256;
+  const int smem = (128 + N) * a.kp * 4 * (SPLIT ? 2 : 1) + 1024 + 256;
   auto fn = k_compose_tc<N, SPLIT>;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) throw std::runtime_error(std::string("compose_tc smem: ") + cudaGetErrorString(e));
@@ -273,9 +315,12 @@ int launch_compose_tc(const float* A, const float* M, const float* Xo, const uin
     N = (int)((I + 31) / 32 * 32);
     if (N > 256) N = 256;
   }
-  while (N > 32 && 2 * (128 + N) * a.kp * 4 * (split3 ? 2 : 1) + 1280 > 200 * 1024) N /= 2;
+  while (N > 32 && (128 + N) * a.kp * 4 * (split3 ? 2 : 1) + 1280 > 200 * 1024) N /= 2;
   if (N != 32 && N != 64 && N != 96 && N != 128 && N != 160 && N != 192 && N != 224 && N != 256) N = 256;
   a.n_rb = (a.rows + 127) / 128;
+  // a tile's 128 rows are one contiguous run of X when rows = i, or rows = p
+  // within one run of the fastest modes (P a multiple of 128)
+  a.prefetch = (!a.rows_are_p || P % 128 == 0) ? 1 : 0;
   const long long n_cb = (a.cols + N - 1) / N;
   a.n_tiles = a.n_rb * n_cb;
   int grid = (int)std::min<long long>(a.n_tiles, n_sm);
