@@ -132,7 +132,8 @@ __global__ void __launch_bounds__(THREADS, 1)
           if (gc >= args.cols) break;
           const long long off = rbase + cstride * gc;
           prefetch_l2(args.Xo + off, (uint32_t)(((nrow * 4) + 15) & ~15LL));
-          if (!args.objective_only) prefetch_l2(args.maskbits + (off >> 5), 16);
+          if (!args.objective_only)
+            prefetch_l2(reinterpret_cast<const void*>(reinterpret_cast<uintptr_t>(args.maskbits + (off >> 5)) & ~uintptr_t(15)), 32);
         }
       }
     }
