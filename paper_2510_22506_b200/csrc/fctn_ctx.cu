@@ -40,12 +40,6 @@ struct CudaError : std::runtime_error {
       throw ::fctn::CudaError(std::string(#call) + " failed: " + cudaGetErrorString(_e));            \
   } while (0)
 
-struct Tables {
-  int64_t* d = nullptr;  // rowA | rowC | colB | colC | kA | kB
-  int64_t rows = 0, cols = 0, K = 0;
-  bool swap = false;
-};
-
 static const int64_t M_ID = 0;  // fixed executor id of the M_k buffer
 
 class Ctx : public Executor {
@@ -89,7 +83,8 @@ class Ctx : public Executor {
   double* dstats = nullptr;  // [n*3 factor stats][4 sums]
   int* dstatus = nullptr;
   double* hstats = nullptr;  // pinned mirror (+ status)
-  std::map<std::string, Tables> tables;
+  double* cscratch = nullptr;  // split-K partials of the generic contraction (fp64 Gram network)
+  int64_t cscratch_cap = 0;
   bool configured = false;
   bool uploaded = false;
 
@@ -187,57 +182,15 @@ class Ctx : public Executor {
     throw std::runtime_error("label not found");
   }
 
-  // offsets of a mixed-radix enumeration over `labs` (first fastest)
-  void enum_offsets(const std::vector<int>& labs, const std::vector<int>& l1, const std::vector<int64_t>& s1,
-                    const std::vector<int>& l2, const std::vector<int64_t>& s2, std::vector<int64_t>& o1,
-                    std::vector<int64_t>& o2) {
-    int64_t cnt = 1;
-    std::vector<int64_t> ext, st1, st2;
-    for (int l : labs) {
-      ext.push_back(sh.extent(l));
-      st1.push_back(stride_in(l1, s1, l));
-      st2.push_back(stride_in(l2, s2, l));
-      cnt *= sh.extent(l);
-    }
-    o1.resize(cnt);
-    o2.resize(cnt);
-    std::vector<int64_t> dig(labs.size(), 0);
-    int64_t a = 0, b = 0;
-    for (int64_t e = 0; e < cnt; ++e) {
-      o1[e] = a;
-      o2[e] = b;
-      for (size_t q = 0; q < labs.size(); ++q) {
-        ++dig[q];
-        a += st1[q];
-        b += st2[q];
-        if (dig[q] < ext[q]) break;
-        a -= st1[q] * ext[q];
-        b -= st2[q] * ext[q];
-        dig[q] = 0;
-      }
-    }
-  }
-
-  static std::string key_of(const ContractOp& op) {
-    std::string k;
-    auto add = [&](const std::vector<int>& v) {
-      for (int x : v) k += std::to_string(x) + ",";
-      k += "|";
-    };
-    add(op.a.labels);
-    add(op.b.labels);
-    add(op.out.labels);
-    return k;
-  }
-
-  Tables& tables_for(const ContractOp& op) {
-    std::string key = key_of(op);
-    auto it = tables.find(key);
-    if (it != tables.end()) return it->second;
+  // Descriptor of out = a (*) b over shared labels for the on-device offset
+  // computation (kernels.cuh ContractDesc).  Rows enumerate the operand that
+  // holds the output's fastest label (coalesced stores), each group sorted
+  // by output stride.
+  ContractDesc desc_for(const ContractOp& op, bool* swapped) const {
     const std::vector<int>& out = op.out.labels;
     std::vector<int64_t> so = strides_of(out);
-    bool fast_in_b = std::find(op.b.labels.begin(), op.b.labels.end(), out[0]) != op.b.labels.end();
-    const LTensor& ra = fast_in_b ? op.b : op.a;  // "row" operand
+    const bool fast_in_b = std::find(op.b.labels.begin(), op.b.labels.end(), out[0]) != op.b.labels.end();
+    const LTensor& ra = fast_in_b ? op.b : op.a;
     const LTensor& cb = fast_in_b ? op.a : op.b;
     std::vector<int64_t> sa = strides_of(ra.labels), sb = strides_of(cb.labels);
     std::vector<int> rfree, cfree, shared;
@@ -250,50 +203,52 @@ class Ctx : public Executor {
     for (int l : cb.labels)
       if (std::find(ra.labels.begin(), ra.labels.end(), l) == ra.labels.end()) cfree.push_back(l);
     auto by_out_stride = [&](std::vector<int>& v) {
-      std::sort(v.begin(), v.end(),
-                [&](int x, int y) { return stride_in(out, so, x) < stride_in(out, so, y); });
+      std::sort(v.begin(), v.end(), [&](int x, int y) { return stride_in(out, so, x) < stride_in(out, so, y); });
     };
     by_out_stride(rfree);
     by_out_stride(cfree);
-    std::vector<int64_t> rowA, rowC, colB, colC, kA, kB;
-    enum_offsets(rfree, ra.labels, sa, out, so, rowA, rowC);
-    enum_offsets(cfree, cb.labels, sb, out, so, colB, colC);
-    enum_offsets(shared, ra.labels, sa, cb.labels, sb, kA, kB);
-    Tables t;
-    t.rows = (int64_t)rowA.size();
-    t.cols = (int64_t)colB.size();
-    t.K = (int64_t)kA.size();
-    t.swap = fast_in_b;
-    int64_t total = 2 * t.rows + 2 * t.cols + 2 * t.K;
-    std::vector<int64_t> h;
-    h.reserve(total);
-    h.insert(h.end(), rowA.begin(), rowA.end());
-    h.insert(h.end(), rowC.begin(), rowC.end());
-    h.insert(h.end(), colB.begin(), colB.end());
-    h.insert(h.end(), colC.begin(), colC.end());
-    h.insert(h.end(), kA.begin(), kA.end());
-    h.insert(h.end(), kB.begin(), kB.end());
-    CK(cudaMalloc(&t.d, total * sizeof(int64_t)));
-    CK(cudaMemcpyAsync(t.d, h.data(), total * sizeof(int64_t), cudaMemcpyHostToDevice, st));
-    CK(cudaStreamSynchronize(st));  // host vector goes out of scope
-    return tables.emplace(key, t).first->second;
+    if (rfree.size() > 12 || cfree.size() > 12 || shared.size() > 12) throw UsageError("too many modes");
+    ContractDesc d;
+    d.nr = (int)rfree.size();
+    d.nc = (int)cfree.size();
+    d.nk = (int)shared.size();
+    d.rows = d.cols = d.K = 1;
+    for (int q = 0; q < d.nr; ++q) {
+      const int l = rfree[q];
+      d.r_ext[q] = sh.extent(l);
+      d.r_sa[q] = stride_in(ra.labels, sa, l);
+      d.r_sc[q] = stride_in(out, so, l);
+      d.rows *= d.r_ext[q];
+    }
+    for (int q = 0; q < d.nc; ++q) {
+      const int l = cfree[q];
+      d.c_ext[q] = sh.extent(l);
+      d.c_sb[q] = stride_in(cb.labels, sb, l);
+      d.c_sc[q] = stride_in(out, so, l);
+      d.cols *= d.c_ext[q];
+    }
+    for (int q = 0; q < d.nk; ++q) {
+      const int l = shared[q];
+      d.k_ext[q] = sh.extent(l);
+      d.k_sa[q] = stride_in(ra.labels, sa, l);
+      d.k_sb[q] = stride_in(cb.labels, sb, l);
+      d.K *= d.k_ext[q];
+    }
+    *swapped = fast_in_b;
+    return d;
   }
 
   void contract(const ContractOp& op) override {
-    Tables& t = tables_for(op);
+    bool sw = false;
+    ContractDesc d = desc_for(op, &sw);
     int pm = pbegin(FCTN_K_MERGE);
-    const void* ra = ptr_of(t.swap ? op.b : op.a);
-    const void* cb = ptr_of(t.swap ? op.a : op.b);
+    const void* ra = ptr_of(sw ? op.b : op.a);
+    const void* cb = ptr_of(sw ? op.a : op.b);
     void* out = ptr_of(op.out);
-    const int64_t* d = t.d;
-    const int64_t *rowA = d, *rowC = d + t.rows, *colB = d + 2 * t.rows, *colC = d + 2 * t.rows + t.cols;
-    const int64_t *kA = d + 2 * t.rows + 2 * t.cols, *kB = kA + t.K;
     if (dtype == FCTN_F64)
-      launch_contract<double>((const double*)ra, (const double*)cb, (double*)out, rowA, rowC, colB, colC, kA, kB,
-                              t.rows, t.cols, t.K, st);
+      launch_contract<double>((const double*)ra, (const double*)cb, (double*)out, d, nullptr, 0, n_sm, st);
     else
-      launch_contract<float>((const float*)ra, (const float*)cb, (float*)out, rowA, rowC, colB, colC, kA, kB,
-                             t.rows, t.cols, t.K, st);
+      launch_contract<float>((const float*)ra, (const float*)cb, (float*)out, d, nullptr, 0, n_sm, st);
     ++launches;
     pend(pm, (double)esize * (op.out.numel(sh) + op.a.numel(sh) + op.b.numel(sh)), 1);
   }
@@ -320,8 +275,9 @@ class Ctx : public Executor {
   void release_shape_buffers() {
     for (auto& kv : bufs) cudaFree(kv.second);
     bufs.clear();
-    for (auto& kv : tables) cudaFree(kv.second.d);
-    tables.clear();
+    cudaFree(cscratch);
+    cscratch = nullptr;
+    cscratch_cap = 0;
     for (size_t k = 0; k < A64.size(); ++k) {
       cudaFree(A64[k]);
       if (dtype == FCTN_F32) cudaFree(Ac[k]);
@@ -432,6 +388,8 @@ class Ctx : public Executor {
     for (int k = 0; k < n; ++k) gcap = std::max(gcap, gram_network_peak(k));
     CK(cudaMalloc(&gnet[0], gcap * sizeof(double)));
     CK(cudaMalloc(&gnet[1], gcap * sizeof(double)));
+    cscratch_cap = std::max<int64_t>(1, 4 * gcap);
+    CK(cudaMalloc(&cscratch, cscratch_cap * sizeof(double)));
     std::vector<int64_t> versions = planner ? planner->versions : std::vector<int64_t>(n, 0);
     planner.reset(new Planner(sh, budget));
     planner->versions = versions;
@@ -491,15 +449,11 @@ class Ctx : public Executor {
       const bool last = q + 1 == rest.size();
       op.out.labels = last ? sh.g_labels(k) : contract_out_labels(op.a.labels, op.b.labels);
       double* out_ptr = last ? G : gnet[ping];
-      Tables& t = tables_for(op);
+      bool sw = false;
+      ContractDesc d = desc_for(op, &sw);
       const double* pa = cur_ptr;
       const double* pb = E64[rest[q]];
-      const double* ra = t.swap ? pb : pa;
-      const double* cb = t.swap ? pa : pb;
-      const int64_t* d = t.d;
-      launch_contract<double>(ra, cb, out_ptr, d, d + t.rows, d + 2 * t.rows, d + 2 * t.rows + t.cols,
-                              d + 2 * t.rows + 2 * t.cols, d + 2 * t.rows + 2 * t.cols + t.K, t.rows, t.cols, t.K,
-                              st);
+      launch_contract<double>(sw ? pb : pa, sw ? pa : pb, out_ptr, d, cscratch, cscratch_cap, n_sm, st);
       ++launches;
       cur = op.out;
       cur_ptr = out_ptr;

@@ -1,8 +1,9 @@
 // K1: generic labeled contraction (merge of factors / partials into M_k,
-// network.py:249-258 over tensor.py:156-200) by offset tables, the generic
+// network.py:249-258 over tensor.py:156-200), the generic
 // permutation, and the dtype conversion.  See DESIGN.md.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdio>
 #include <stdexcept>
 #include <string>
@@ -17,29 +18,61 @@ static void check_launch(const char* what) {
 }
 
 // ============================================================ K1 contract
+//
+// C[r, c] = sum_k A[r, k] B[c, k] where r, c, k are mixed-radix multi-indices
+// over labels (ContractDesc): every offset is computed on device from the
+// extents/strides, so a new visiting order or rank table needs no host
+// tables.  Rows enumerate the operand holding C's fastest label, so the
+// stores are coalesced.  Small-output / long-K contractions (the doubled
+// network of the Gram) split K over CTAs and reduce in a fixed order.
+
+__device__ __forceinline__ void md_offsets(int64_t idx, int nd, const int64_t* ext, const int64_t* s1,
+                                           const int64_t* s2, int64_t& o1, int64_t& o2) {
+  o1 = 0;
+  o2 = 0;
+  for (int q = 0; q < nd; ++q) {
+    const int64_t d = idx % ext[q];
+    idx /= ext[q];
+    o1 += d * s1[q];
+    o2 += d * s2[q];
+  }
+}
 
 template <typename T>
 __global__ void __launch_bounds__(256) k_contract(const T* __restrict__ A, const T* __restrict__ B,
-                                                  T* __restrict__ C, const int64_t* __restrict__ rowA,
-                                                  const int64_t* __restrict__ rowC,
-                                                  const int64_t* __restrict__ colB,
-                                                  const int64_t* __restrict__ colC,
-                                                  const int64_t* __restrict__ kA,
-                                                  const int64_t* __restrict__ kB, int64_t rows,
-                                                  int64_t cols, int64_t K, int64_t tiles_r) {
+                                                  T* __restrict__ C, T* __restrict__ part, const ContractDesc d,
+                                                  int64_t tiles_r, int64_t kchunk) {
   constexpr int BR = 64, BC = 64, KC = 16;
   __shared__ T As[KC][BR + 1];
   __shared__ T Bs[KC][BC + 1];
-  __shared__ int64_t sRA[BR], sCB[BC];
+  __shared__ int64_t sRA[BR], sRC[BR], sCB[BC], sCC[BC];
+  extern __shared__ int64_t sK[];  // [kA | kB] for this CTA's K range
   const int64_t tile = blockIdx.x;
   const int64_t r0 = (tile % tiles_r) * BR;
   const int64_t c0 = (tile / tiles_r) * BC;
+  const int64_t kb = blockIdx.y * kchunk;
+  int64_t ke = kb + kchunk;
+  if (ke > d.K) ke = d.K;
+  const int64_t nk = ke - kb;
   const int tid = threadIdx.x;
   if (tid < BR) {
-    sRA[tid] = (r0 + tid < rows) ? rowA[r0 + tid] : -1;
+    const int64_t r = r0 + tid;
+    int64_t oa = -1, oc = 0;
+    if (r < d.rows) md_offsets(r, d.nr, d.r_ext, d.r_sa, d.r_sc, oa, oc);
+    sRA[tid] = oa;
+    sRC[tid] = oc;
   } else if (tid < BR + BC) {
-    int c = tid - BR;
-    sCB[c] = (c0 + c < cols) ? colB[c0 + c] : -1;
+    const int c = tid - BR;
+    int64_t ob = -1, oc = 0;
+    if (c0 + c < d.cols) md_offsets(c0 + c, d.nc, d.c_ext, d.c_sb, d.c_sc, ob, oc);
+    sCB[c] = ob;
+    sCC[c] = oc;
+  }
+  for (int64_t k = tid; k < nk; k += 256) {
+    int64_t oa, ob;
+    md_offsets(kb + k, d.nk, d.k_ext, d.k_sa, d.k_sb, oa, ob);
+    sK[k] = oa;
+    sK[nk + k] = ob;
   }
   __syncthreads();
   const int tx = tid & 15, ty = tid >> 4;
@@ -48,20 +81,16 @@ __global__ void __launch_bounds__(256) k_contract(const T* __restrict__ A, const
   for (int a = 0; a < 4; ++a)
 #pragma unroll
     for (int b = 0; b < 4; ++b) acc[a][b] = T(0);
-  for (int64_t k0 = 0; k0 < K; k0 += KC) {
+  for (int64_t k0 = 0; k0 < nk; k0 += KC) {
     for (int e = tid; e < KC * BR; e += 256) {
-      int kk = e / BR, r = e % BR;
-      int64_t ra = sRA[r];
-      T v = T(0);
-      if (ra >= 0 && k0 + kk < K) v = A[ra + kA[k0 + kk]];
-      As[kk][r] = v;
+      const int kk = e / BR, r = e % BR;
+      const int64_t ra = sRA[r];
+      As[kk][r] = (ra >= 0 && k0 + kk < nk) ? A[ra + sK[k0 + kk]] : T(0);
     }
     for (int e = tid; e < KC * BC; e += 256) {
-      int kk = e / BC, c = e % BC;
-      int64_t cb = sCB[c];
-      T v = T(0);
-      if (cb >= 0 && k0 + kk < K) v = B[cb + kB[k0 + kk]];
-      Bs[kk][c] = v;
+      const int kk = e / BC, c = e % BC;
+      const int64_t cb = sCB[c];
+      Bs[kk][c] = (cb >= 0 && k0 + kk < nk) ? B[cb + sK[nk + k0 + kk]] : T(0);
     }
     __syncthreads();
 #pragma unroll
@@ -80,33 +109,74 @@ __global__ void __launch_bounds__(256) k_contract(const T* __restrict__ A, const
   }
 #pragma unroll
   for (int a = 0; a < 4; ++a) {
-    int64_t r = r0 + tx + 16 * a;
-    if (r >= rows) continue;
-    int64_t rc = rowC[r];
+    const int rl = tx + 16 * a;
+    if (r0 + rl >= d.rows) continue;
 #pragma unroll
     for (int b = 0; b < 4; ++b) {
-      int64_t c = c0 + ty + 16 * b;
-      if (c < cols) C[rc + colC[c]] = acc[a][b];
+      const int cl = ty + 16 * b;
+      if (c0 + cl >= d.cols) continue;
+      if (part)
+        part[blockIdx.y * d.rows * d.cols + (r0 + rl) + d.rows * (c0 + cl)] = acc[a][b];
+      else
+        C[sRC[rl] + sCC[cl]] = acc[a][b];
     }
   }
 }
 
 template <typename T>
-void launch_contract(const T* A, const T* B, T* C, const int64_t* rowA, const int64_t* rowC,
-                     const int64_t* colB, const int64_t* colC, const int64_t* kA, const int64_t* kB,
-                     int64_t rows, int64_t cols, int64_t K, cudaStream_t st) {
-  int64_t tr = (rows + 63) / 64, tc = (cols + 63) / 64;
-  int64_t tiles = tr * tc;
-  if (tiles <= 0) return;
-  k_contract<T><<<(unsigned)tiles, 256, 0, st>>>(A, B, C, rowA, rowC, colB, colC, kA, kB, rows, cols, K, tr);
-  check_launch("contract");
+__global__ void k_contract_reduce(const T* __restrict__ part, int nsplit, const ContractDesc d, T* __restrict__ C) {
+  const int64_t n = d.rows * d.cols;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+    T v = T(0);
+    for (int s = 0; s < nsplit; ++s) v += part[s * n + e];
+    int64_t x, rc, cc;
+    md_offsets(e % d.rows, d.nr, d.r_ext, d.r_sa, d.r_sc, x, rc);
+    md_offsets(e / d.rows, d.nc, d.c_ext, d.c_sb, d.c_sc, x, cc);
+    C[rc + cc] = v;
+  }
 }
-template void launch_contract<double>(const double*, const double*, double*, const int64_t*, const int64_t*,
-                                      const int64_t*, const int64_t*, const int64_t*, const int64_t*, int64_t,
-                                      int64_t, int64_t, cudaStream_t);
-template void launch_contract<float>(const float*, const float*, float*, const int64_t*, const int64_t*,
-                                     const int64_t*, const int64_t*, const int64_t*, const int64_t*, int64_t,
-                                     int64_t, int64_t, cudaStream_t);
+
+int64_t contract_split_scratch(const ContractDesc& d, int n_sm) {
+  const int64_t tiles = ((d.rows + 63) / 64) * ((d.cols + 63) / 64);
+  if (tiles >= n_sm || d.K < 256) return 0;
+  int64_t ns = std::min<int64_t>(d.K / 64, (2 * n_sm + tiles - 1) / tiles);
+  if (ns < 2) return 0;
+  return ns * d.rows * d.cols;
+}
+
+template <typename T>
+void launch_contract(const T* A, const T* B, T* C, const ContractDesc& d, T* scratch, int64_t scratch_cap, int n_sm,
+                     cudaStream_t st) {
+  const int64_t tr = (d.rows + 63) / 64, tcn = (d.cols + 63) / 64;
+  const int64_t tiles = tr * tcn;
+  if (tiles <= 0) return;
+  int64_t ns = 1;
+  if (scratch && tiles < n_sm && d.K >= 256) {
+    ns = std::min<int64_t>(d.K / 64, (2 * n_sm + tiles - 1) / tiles);
+    while (ns > 1 && ns * d.rows * d.cols > scratch_cap) --ns;
+  }
+  int64_t kchunk = (d.K + ns - 1) / ns;
+  ns = (d.K + kchunk - 1) / kchunk;
+  if (kchunk > 6144) throw std::runtime_error("contraction K chunk too long for the on-chip offset table");
+  const size_t smem = (size_t)2 * kchunk * sizeof(int64_t);
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(k_contract<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem + 1024);
+    if (e != cudaSuccess) throw std::runtime_error(std::string("contract smem: ") + cudaGetErrorString(e));
+  }
+  dim3 grid((unsigned)tiles, (unsigned)ns);
+  k_contract<T><<<grid, 256, smem, st>>>(A, B, C, ns > 1 ? scratch : nullptr, d, tr, kchunk);
+  check_launch("contract");
+  if (ns > 1) {
+    const int64_t n = d.rows * d.cols;
+    int64_t blocks = std::min<int64_t>((n + 255) / 256, 4 * n_sm);
+    k_contract_reduce<T><<<(unsigned)blocks, 256, 0, st>>>(scratch, (int)ns, d, C);
+    check_launch("contract_reduce");
+  }
+}
+template void launch_contract<double>(const double*, const double*, double*, const ContractDesc&, double*, int64_t,
+                                      int, cudaStream_t);
+template void launch_contract<float>(const float*, const float*, float*, const ContractDesc&, float*, int64_t, int,
+                                     cudaStream_t);
 
 template <typename T>
 __global__ void k_permute(const T* __restrict__ in, T* __restrict__ out, PermDesc d, int64_t numel) {

@@ -9,12 +9,21 @@
 namespace fctn {
 
 // ---------------------------------------------------------------- K1 merge
-// Generic labeled contraction via offset tables (network.py:249-258,
-// tensor.py:156-200).  C[rowC[r]+colC[c]] = sum_k A[rowA[r]+kA[k]] * B[colB[c]+kB[k]].
+// Generic labeled contraction (network.py:249-258, tensor.py:156-200):
+// C[rc(r)+cc(c)] = sum_k A[ra(r)+ka(k)] * B[cb(c)+kb(k)], each offset a
+// mixed-radix multi-index over the labels (up to 12 per group).
+struct ContractDesc {
+  int nr = 0, nc = 0, nk = 0;
+  int64_t r_ext[12], r_sa[12], r_sc[12];
+  int64_t c_ext[12], c_sb[12], c_sc[12];
+  int64_t k_ext[12], k_sa[12], k_sb[12];
+  int64_t rows = 1, cols = 1, K = 1;
+};
+// scratch: split-K partials (may be null: no split); returns nothing
 template <typename T>
-void launch_contract(const T* A, const T* B, T* C, const int64_t* rowA, const int64_t* rowC,
-                     const int64_t* colB, const int64_t* colC, const int64_t* kA, const int64_t* kB,
-                     int64_t rows, int64_t cols, int64_t K, cudaStream_t st);
+void launch_contract(const T* A, const T* B, T* C, const ContractDesc& d, T* scratch, int64_t scratch_cap, int n_sm,
+                     cudaStream_t st);
+int64_t contract_split_scratch(const ContractDesc& d, int n_sm);
 
 // generic permutation: out[o] = in[sum_d digit_d(o) * in_stride[d]]
 struct PermDesc {
