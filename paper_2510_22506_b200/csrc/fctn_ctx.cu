@@ -87,6 +87,11 @@ class Ctx : public Executor {
   int64_t cscratch_cap = 0;
   bool configured = false;
   bool uploaded = false;
+  // N = 3 schedule (see compute_z0): Z_0 = X x_0 A_(0) and its A_0 version
+  void* Zbuf = nullptr;
+  int64_t z_version = -1;
+  int mbuf_holds = -1;   // mode whose M_k currently sits in Mbuf (-1: none)
+  bool zroute = true;    // FCTN_NO_ZROUTE=1 disables
 
   // profiling: events bracketing launch groups, accumulated per class
   struct Mark {
@@ -284,8 +289,10 @@ class Ctx : public Executor {
     }
     A64.clear();
     Ac.clear();
-    for (auto* p : {Ascratch, (double*)Mbuf, Y, G, Fr, Fi, ypart, partials, epart, colstats, gnet[0], gnet[1]})
+    for (auto* p : {Ascratch, (double*)Mbuf, (double*)Zbuf, Y, G, Fr, Fi, ypart, partials, epart, colstats, gnet[0],
+                     gnet[1]})
       cudaFree(p);
+    Zbuf = nullptr;
     for (auto* p : E64) cudaFree(p);
     E64.clear();
     Ascratch = nullptr;
@@ -375,6 +382,9 @@ class Ctx : public Executor {
     }
     CK(cudaMalloc(&Ascratch, max_is * sizeof(double)));
     CK(cudaMalloc(&Mbuf, max_m * esize));
+    if (n == 3) CK(cudaMalloc(&Zbuf, std::max<int64_t>(1, sh.s_of(0) * (T / sh.dims[0])) * esize));
+    z_version = -1;
+    mbuf_holds = -1;
     CK(cudaMalloc(&Y, max_is * sizeof(double)));
     CK(cudaMalloc(&G, max_ss * sizeof(double)));
     CK(cudaMalloc(&Fr, max_h * sizeof(double)));
@@ -388,7 +398,7 @@ class Ctx : public Executor {
     for (int k = 0; k < n; ++k) gcap = std::max(gcap, gram_network_peak(k));
     CK(cudaMalloc(&gnet[0], gcap * sizeof(double)));
     CK(cudaMalloc(&gnet[1], gcap * sizeof(double)));
-    cscratch_cap = std::max<int64_t>(1, 4 * gcap);
+    cscratch_cap = std::max<int64_t>(std::max<int64_t>(1, 4 * gcap), (int64_t)(2 * n_sm + 8) * max_is);
     CK(cudaMalloc(&cscratch, cscratch_cap * sizeof(double)));
     std::vector<int64_t> versions = planner ? planner->versions : std::vector<int64_t>(n, 0);
     planner.reset(new Planner(sh, budget));
@@ -501,6 +511,8 @@ class Ctx : public Executor {
     {
       const char* e = getenv("FCTN_NO_TC");
       use_tc = !(e && e[0] == '1');
+      const char* zr = getenv("FCTN_NO_ZROUTE");
+      zroute = !(zr && zr[0] == '1');
       const char* t = getenv("FCTN_TF32");
       split3 = !(t && std::string(t) == "1x");
     }
@@ -559,7 +571,106 @@ class Ctx : public Executor {
   }
 
   // ------------------------------------------------------------ sweep pieces
+  // ------------------------------------------------------------ N = 3 schedule
+  // For three modes the reference's reuse cache never stores anything
+  // (network.py:436-438,473) and M_k of a short mode is as large as X
+  // (c4: M_2 is 268 M entries).  There Y_k is formed without M_k:
+  //   Z_0 = X x_0 A_(0)  (one tensor-core pass over X, contracting the
+  //                       contiguous mode; T s_0 / I_0 entries),
+  //   Y_k = Z_0 (*) A_(l) (a small contraction over i_l and the bond (0,l)),
+  // the same sums as X_(k) M_k^T in another association.  Z_0 stays valid
+  // while A_0 and X are unchanged, so in orders where mode 0 comes first both
+  // other updates share one pass over X.  The FLOP / cache counters still
+  // come from the planner's replay of the reference chain.
+  bool z_route(int k) const {
+    if (sh.n != 3 || k == 0 || !zroute || !Zbuf) return false;
+    if (dtype == FCTN_F32 && !(use_tc && tc_stream_supported(sh.total() / sh.dims[0], sh.dims[0], 1, sh.s_of(0))))
+      return false;
+    if (z_version == planner->versions[0]) return true;  // fresh: no pass over X at all
+    const int64_t T = sh.total();
+    const int64_t mk = sh.s_of(k) * (T / sh.dims[k]);
+    const int64_t z0 = sh.s_of(0) * (T / sh.dims[0]);
+    return 4 * z0 <= mk;
+  }
+  std::vector<int> z_labels() const {
+    std::vector<int> out;
+    for (int j = 1; j < sh.n; ++j) out.push_back(j);
+    for (int b : sh.bonds_of(0)) out.push_back(b);
+    return out;
+  }
+  void compute_z0() {
+    const int64_t T = sh.total();
+    const int64_t I0 = sh.dims[0], p0 = T / I0, S0 = sh.s_of(0);
+    int pm = pbegin(FCTN_K_STREAM_Y);
+    if (dtype == FCTN_F32) {
+      // the stream kernel with the roles of the modes swapped: rows = (i1, i2),
+      // K = i0 (X's contiguous mode, K-major tiles), B = A_(0)
+      TcStreamPlan tp = plan_stream_tc(p0, I0, 1, S0, n_sm, split3);
+      tp.kb_per_split = tp.nkb;
+      tp.nsplit = 1;
+      launch_stream_tc((const float*)X[cur], (const float*)Ac[0], (float*)Zbuf, p0, I0, 1, S0, tp, st);
+    } else {
+      StreamPlan sp = plan_stream(p0, S0, I0, target_ctas());
+      launch_stream<double>((const double*)X[cur], (const double*)Ac[0], ypart, p0, I0, S0, I0, sp, st);
+      launch_reduce_splits(ypart, sp.nsplit, p0 * S0, nullptr, 0.0, (double*)Zbuf, st);
+      ++launches;
+    }
+    ++launches;
+    pend(pm, (double)esize * (T + I0 * S0 + p0 * S0), 1);
+    z_version = planner->versions[0];
+  }
+  void y_from_z(int k) {
+    int l = 0;
+    for (int j = 1; j < 3; ++j)
+      if (j != k) l = j;
+    const int64_t I = sh.dims[k], S = sh.s_of(k);
+    ContractOp op;
+    op.a.labels = z_labels();
+    op.b.labels = sh.factor_labels(l);
+    op.out.labels = sh.factor_labels(k);
+    bool sw = false;
+    ContractDesc d = desc_for(op, &sw);
+    int pm = pbegin(FCTN_K_STREAM_Y);
+    if (dtype == FCTN_F32) {
+      const float *pa = (const float*)Zbuf, *pb = (const float*)Ac[l];
+      launch_contract<float>(sw ? pb : pa, sw ? pa : pb, (float*)ypart, d, (float*)cscratch, 2 * cscratch_cap, n_sm, st);
+      launch_reduce_splits_f32((const float*)ypart, 1, I * S, A64[k], rho, Y, st);
+    } else {
+      const double *pa = (const double*)Zbuf, *pb = A64[l];
+      launch_contract<double>(sw ? pb : pa, sw ? pa : pb, ypart, d, cscratch, cscratch_cap, n_sm, st);
+      launch_reduce_splits(ypart, 1, I * S, A64[k], rho, Y, st);
+    }
+    launches += 3;
+    pend(pm, (double)esize * (d.rows * d.cols + (sh.total() / sh.dims[0]) * sh.s_of(0)), 3);
+  }
+  // M_j of the current factors into Mbuf, outside the reference's chain (no meter)
+  void build_m_direct(int k) {
+    std::vector<int> rest;
+    for (int j = 0; j < sh.n; ++j)
+      if (j != k) rest.push_back(j);
+    if (rest.size() != 2) throw std::runtime_error("direct M build is for three modes");
+    ContractOp op;
+    op.a.labels = sh.factor_labels(rest[0]);
+    op.a.factor = rest[0];
+    op.b.labels = sh.factor_labels(rest[1]);
+    op.b.factor = rest[1];
+    op.out.labels = sh.m_labels(k);
+    op.out.buf = M_ID;
+    contract(op);
+    mbuf_holds = k;
+  }
+
   void factor_update(int k, int extrap, double alpha, double beta) {
+    if (z_route(k)) {
+      if (z_version != planner->versions[0]) compute_z0();
+      y_from_z(k);
+    } else {
+      y_stream(k);
+    }
+    solve_factor(k, extrap, alpha, beta);
+  }
+
+  void y_stream(int k) {
     const int64_t T = sh.total();
     const int64_t I = sh.dims[k], S = sh.s_of(k), p = T / I;
     int64_t P = 1;
@@ -587,8 +698,13 @@ class Ctx : public Executor {
     else
       launch_reduce_splits(ypart, nsplit, I * S, A64[k], rho, Y, st);
     pend(pm, (tc ? 4.0 : 8.0) * nsplit * I * S + 16.0 * I * S, 1);
+  }
+
+  void solve_factor(int k, int extrap, double alpha, double beta) {
+    const int64_t T = sh.total();
+    const int64_t I = sh.dims[k], S = sh.s_of(k), p = T / I;
     // G_k = M_k M_k^T by the doubled network (sylvester.py:57-59)
-    pm = pbegin(FCTN_K_GRAM);
+    int pm = pbegin(FCTN_K_GRAM);
     int64_t l0 = launches;
     gram_network(k);
     pend(pm, 8.0 * S * S, launches - l0);
@@ -608,6 +724,7 @@ class Ctx : public Executor {
                             delta[k], sgn, colstats, st);
     launch_factor_gram(Ascratch, I, S, epart, E64[k], colstats, dstats + 3 * k, st);
     pend(pm, 8.0 * (4.0 * I * S + 2.0 * dp.H1 * S + S * S), 5);
+    if (mbuf_holds >= 0 && mbuf_holds != k) mbuf_holds = -1;  // M_j (j != k) contains A_k
     std::swap(A64[k], Ascratch);
     if (dtype == FCTN_F64) Ac[k] = A64[k];
     launches += 7;
@@ -669,16 +786,27 @@ class Ctx : public Executor {
     launches = 0;
     CK(cudaEventRecord(ev0, st));
     for (int k : order) {
-      if (alg == FCTN_ALG_ACCEL)
-        planner->partial_cached(k, order, this, M_ID);
-      else
-        planner->partial_plain(k, this, M_ID);
+      const bool zr = z_route(k);
+      if (alg == FCTN_ALG_ACCEL) {
+        planner->partial_cached(k, order, zr ? nullptr : this, M_ID);  // dry replay when M_k is not needed
+      } else {
+        planner->partial_plain(k, zr ? nullptr : this, M_ID);
+      }
+      mbuf_holds = zr ? -1 : k;
       factor_update(k, extrap, alpha, beta);
     }
     int k_last = order.back();
     if (alg == FCTN_ALG_ACCEL) {
       planner->meter.compose += 2 * (sh.total() / sh.dims[k_last]) * sh.s_of(k_last) * sh.dims[k_last];
-      compose(k_last, false);
+      int kc = k_last;
+      if (sh.n == 3 && zroute) {
+        // compose through the mode with the smallest M_j (same product, another association)
+        const int64_t T = sh.total();
+        for (int j = 0; j < 3; ++j)
+          if (sh.s_of(j) * (T / sh.dims[j]) < sh.s_of(kc) * (T / sh.dims[kc])) kc = j;
+        if (mbuf_holds != kc) build_m_direct(kc);
+      }
+      compose(kc, false);
     } else {
       // compose(f): the chain's FLOPs (network.py:271-278); on device the full
       // tensor is A_(n-1) times the plain partial around n-1.
@@ -691,6 +819,8 @@ class Ctx : public Executor {
     CK(cudaEventRecord(ev1, st));
     fetch_stats();
     cur ^= 1;
+    z_version = -1;  // X changed
+    mbuf_holds = -1;
     float ms = 0.f;
     CK(cudaEventElapsedTime(&ms, ev0, ev1));
     double pen = 0.0, step = 0.0, fmax = 0.0;
@@ -727,6 +857,7 @@ class Ctx : public Executor {
     Meter keep = planner->meter;
     planner->partial_plain(0, this, M_ID);
     planner->meter = keep;
+    mbuf_holds = -1;
     compose(0, true);
     fetch_stats();
     double val = 0.5 * hstats[3 * n + 2];
@@ -795,6 +926,8 @@ int fctn_upload(fctn_ctx* c, const void* x_F, const uint8_t* mask_F) {
     CK(cudaStreamSynchronize(x.st));
     x.cur = 0;
     x.uploaded = true;
+    x.z_version = -1;
+    x.mbuf_holds = -1;
   });
 }
 
@@ -808,6 +941,8 @@ int fctn_set_factors(fctn_ctx* c, const double* const* a_unf, const int64_t* ver
       if (versions) x.planner->versions[k] = versions[k];
     }
     for (int k = 0; k < x.sh.n; ++k) x.factor_refresh(k);
+    x.z_version = -1;
+    x.mbuf_holds = -1;
     if (reset_cache) x.planner->reset_cache(&x);
     CK(cudaStreamSynchronize(x.st));
   });
