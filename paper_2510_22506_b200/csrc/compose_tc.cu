@@ -11,10 +11,11 @@
 // operand stage and a double-buffered TMEM accumulator, so the MMA of tile
 // t+1 overlaps the epilogue of tile t; the producer also bulk-prefetches each
 // tile's X_old rows into L2 so the epilogue's loads hit L2.
-// Warp roles (704 threads): warp 0 TMA + L2 prefetch, warp 1 TMEM alloc +
-// MMA issue, warps 2..5 TF32 rounding / 3xTF32 split of the landed operand
-// tiles, warps 6..21 epilogue (four warps per TMEM lane quadrant, column
-// quarters).
+// Warp roles (704 threads): warp 0 TMA (lane 0) + L2 prefetch (all lanes),
+// warp 1 TMEM alloc + MMA issue, warps 2..5 TF32 rounding / 3xTF32 split of
+// operand tiles that were not pre-split in HBM, warps 6..21 epilogue (four
+// warps per TMEM lane quadrant, column quarters).  K = s runs through a ring
+// of 32-row stages.
 // The observation mask is read bit-packed (1 bit per entry, F order).
 #include <cuda.h>
 #include <cudaTypedefs.h>
@@ -34,9 +35,11 @@ CUtensorMap tc_make_map_f32(const void* base, int rank, const uint64_t* dims, co
 
 namespace {
 
+constexpr int KB = 32;  // K rows per pipeline stage
 constexpr int CONV_WARPS = 4;
 constexpr int EPI_WARPS = 16;
-constexpr int EPI0 = 2 + CONV_WARPS;  // first epilogue warp
+constexpr int CONV0 = 2;                       // first converter warp
+constexpr int EPI0 = CONV0 + CONV_WARPS;       // first epilogue warp
 constexpr int NWARPS = EPI0 + EPI_WARPS;
 constexpr int THREADS = 32 * NWARPS;
 
@@ -48,9 +51,11 @@ struct ComposeArgs {
   long long rows, cols;       // accumulator extents (row axis = contiguous axis of X_(k))
   long long n_rb, n_tiles;
   long long P, PI, I;         // X view
-  int kp;                     // K (= s padded to 8)
+  int nkb;                    // K blocks per tile (s padded to 32)
+  int stages;
   int rows_are_p;
   int prefetch;               // rows of a tile are contiguous in X: bulk-prefetch them to L2
+  int a_pre, b_pre;           // operand arrives pre-split (hi and lo tensors) from HBM
   float rho, onep;
   int objective_only;
 };
@@ -66,21 +71,24 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
+// Stage layout: [A hi | B hi | A lo | B lo]; A = 128 rows, B = N cols, each
+// a set of 32 x 32 MN-major boxes (4 KB, SWIZZLE_128B_BASE32B).
 template <int N, bool SPLIT>
 __global__ void __launch_bounds__(THREADS, 1)
-    k_compose_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+    k_compose_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmAl,
+                 const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUtensorMap tmBl,
                  const ComposeArgs args) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  const int kp = args.kp;
-  const uint32_t a_bytes = 128u * kp * 4u, b_bytes = (uint32_t)N * kp * 4u;
-  const uint32_t tma_bytes = a_bytes + b_bytes;
-  const uint32_t stage_bytes = tma_bytes * (SPLIT ? 2 : 1);  // [A hi | B hi | (A lo | B lo)]
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + stage_bytes);
-  uint64_t* conv = full + 1;
-  uint64_t* empty = conv + 1;
-  uint64_t* tfull = empty + 1;   // [2]
-  uint64_t* tempty = tfull + 2;  // [2]
+  constexpr uint32_t A_B = 128u * KB * 4u, B_B = (uint32_t)N * KB * 4u;
+  constexpr uint32_t HI = A_B + B_B;
+  constexpr uint32_t STAGE = HI * (SPLIT ? 2 : 1);
+  const int S_ = args.stages;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S_ * STAGE);
+  uint64_t* conv = full + S_;
+  uint64_t* empty = conv + S_;
+  uint64_t* tfull = empty + S_;   // [2]
+  uint64_t* tempty = tfull + 2;   // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
   __shared__ double red[4][NWARPS];
 
@@ -90,9 +98,11 @@ __global__ void __launch_bounds__(THREADS, 1)
   if (warp == 0 && lane == 0) {
     tc::tma_prefetch(&tmA);
     tc::tma_prefetch(&tmB);
-    tc::mbar_init(full, 1);
-    tc::mbar_init(conv, CONV_WARPS);
-    tc::mbar_init(empty, 1);
+    for (int s = 0; s < S_; ++s) {
+      tc::mbar_init(&full[s], 1);
+      tc::mbar_init(&conv[s], CONV_WARPS);
+      tc::mbar_init(&empty[s], 1);
+    }
     for (int s = 0; s < 2; ++s) {
       tc::mbar_init(&tfull[s], 1);
       tc::mbar_init(&tempty[s], EPI_WARPS);
@@ -106,71 +116,95 @@ __global__ void __launch_bounds__(THREADS, 1)
   const uint32_t tmem = *tmem_slot;
   double s_d = 0.0, s_b = 0.0, s_c = 0.0, s_n = 0.0;
 
-  if (warp == 0 && lane == 0) {
-    // ---- TMA producer (one operand stage: the K = s MMA is short, the TMEM
-    // double buffer is what overlaps tile t+1's MMA with tile t's epilogue)
-    int j = 0;
-    for (long long t = blockIdx.x; t < args.n_tiles; t += gridDim.x, ++j) {
-      tc::mbar_wait(empty, (j & 1) ^ 1);
-      tc::mbar_expect_tx(full, tma_bytes);
-      const long long rb = t % args.n_rb, cb = t / args.n_rb;
-      const int r0 = (int)(rb * 128), c0 = (int)(cb * N);
-      uint8_t* a = smem;
-      uint8_t* b = a + a_bytes;
-      const uint32_t chunk = 32u * kp * 4u;
+  if (warp == 0) {
+    // ---- TMA producer (lane 0) + L2 prefetch of each tile's X_old rows and
+    // mask words (all lanes, paced by the stage ring, so ~one tile ahead of
+    // the MMA and two ahead of the epilogue)
+    uint32_t tx = HI;
+    if (SPLIT) tx += (args.a_pre ? A_B : 0) + (args.b_pre ? B_B : 0);
+    int g = 0;
+    for (long long t = blockIdx.x; t < args.n_tiles; t += gridDim.x) {
+      const int r0 = (int)((t % args.n_rb) * 128), c0 = (int)((t / args.n_rb) * N);
+      if (lane == 0) {
+        for (int kb = 0; kb < args.nkb; ++kb, ++g) {
+          const int s = g % S_;
+          tc::mbar_wait(&empty[s], ((g / S_) & 1) ^ 1);
+          tc::mbar_expect_tx(&full[s], tx);
+          uint8_t* st = smem + s * STAGE;
 #pragma unroll
-      for (int c = 0; c < 4; ++c) tc::tma_load_2d(a + c * chunk, &tmA, full, r0 + 32 * c, 0);
+          for (int c = 0; c < 4; ++c) tc::tma_load_2d(st + c * 4096, &tmA, &full[s], r0 + 32 * c, kb * KB);
 #pragma unroll
-      for (int c = 0; c < N / 32; ++c) tc::tma_load_2d(b + c * chunk, &tmB, full, c0 + 32 * c, 0);
+          for (int c = 0; c < N / 32; ++c)
+            tc::tma_load_2d(st + A_B + c * 4096, &tmB, &full[s], c0 + 32 * c, kb * KB);
+          if (SPLIT && args.a_pre)
+#pragma unroll
+            for (int c = 0; c < 4; ++c) tc::tma_load_2d(st + HI + c * 4096, &tmAl, &full[s], r0 + 32 * c, kb * KB);
+          if (SPLIT && args.b_pre)
+#pragma unroll
+            for (int c = 0; c < N / 32; ++c)
+              tc::tma_load_2d(st + HI + A_B + c * 4096, &tmBl, &full[s], c0 + 32 * c, kb * KB);
+        }
+      }
+      __syncwarp();
       if (args.prefetch) {
-        // stream this tile's X_old rows (and mask words) into L2 ahead of the epilogue
         const long long rbase = args.rows_are_p ? (r0 % args.P) + args.PI * (r0 / args.P) : r0;
         const long long cstride = args.rows_are_p ? args.P : args.I;
         const long long nrow = args.rows - r0 < 128 ? args.rows - r0 : 128;
-        for (int c = 0; c < N; ++c) {
+        for (int c = lane; c < N; c += 32) {
           const long long gc = c0 + c;
           if (gc >= args.cols) break;
           const long long off = rbase + cstride * gc;
           prefetch_l2(args.Xo + off, (uint32_t)(((nrow * 4) + 15) & ~15LL));
           if (!args.objective_only)
-            prefetch_l2(reinterpret_cast<const void*>(reinterpret_cast<uintptr_t>(args.maskbits + (off >> 5)) & ~uintptr_t(15)), 32);
+            prefetch_l2(reinterpret_cast<const void*>(reinterpret_cast<uintptr_t>(args.maskbits + (off >> 5)) &
+                                                      ~uintptr_t(15)),
+                        32);
         }
       }
     }
   } else if (warp == 1 && lane == 0) {
     // ---- MMA issuer
     constexpr uint32_t idesc = tc::idesc_tf32(128, N, true, true);
-    const uint32_t chunk = 32u * kp * 4u;
-    int j = 0;
+    int g = 0, j = 0;
     for (long long t = blockIdx.x; t < args.n_tiles; t += gridDim.x, ++j) {
-      const int s = j & 1;
-      tc::mbar_wait(&tempty[s], ((j >> 1) & 1) ^ 1);
-      tc::mbar_wait(conv, j & 1);
-      tc::fence_after_sync();
-      const uint32_t a = tc::smem_u32(smem);
-      const uint32_t b = a + a_bytes;
-      for (int kk = 0; kk < kp / 8; ++kk) {
-        const uint64_t ad = tc::sdesc(a + kk * 1024, chunk, 512, 1);
-        const uint64_t bd = tc::sdesc(b + kk * 1024, chunk, 512, 1);
-        if (SPLIT) {
-          tc::mma_tf32(tmem + s * N, tc::sdesc(a + tma_bytes + kk * 1024, chunk, 512, 1), bd, idesc, kk != 0);
-          tc::mma_tf32(tmem + s * N, ad, tc::sdesc(b + tma_bytes + kk * 1024, chunk, 512, 1), idesc, 1);
+      const int acc = j & 1;
+      tc::mbar_wait(&tempty[acc], ((j >> 1) & 1) ^ 1);
+      for (int kb = 0; kb < args.nkb; ++kb, ++g) {
+        const int s = g % S_;
+        tc::mbar_wait(&conv[s], (g / S_) & 1);
+        tc::fence_after_sync();
+        const uint32_t a = tc::smem_u32(smem + s * STAGE), b = a + A_B;
+#pragma unroll
+        for (int kk = 0; kk < KB / 8; ++kk) {
+          const uint64_t ad = tc::sdesc(a + kk * 1024, 4096, 512, 1);
+          const uint64_t bd = tc::sdesc(b + kk * 1024, 4096, 512, 1);
+          const uint32_t first = (kb | kk) != 0;
+          if (SPLIT) {
+            tc::mma_tf32(tmem + acc * N, tc::sdesc(a + HI + kk * 1024, 4096, 512, 1), bd, idesc, first);
+            tc::mma_tf32(tmem + acc * N, ad, tc::sdesc(b + HI + kk * 1024, 4096, 512, 1), idesc, 1);
+          }
+          tc::mma_tf32(tmem + acc * N, ad, bd, idesc, SPLIT ? 1u : first);
         }
-        tc::mma_tf32(tmem + s * N, ad, bd, idesc, SPLIT || kk != 0);
+        tc::mma_commit(&empty[s]);
       }
-      tc::mma_commit(empty);
-      tc::mma_commit(&tfull[s]);
+      tc::mma_commit(&tfull[acc]);
     }
-  } else if (warp >= 2 && warp < EPI0) {
-    // ---- operand rounding (TF32 round-to-nearest) or 3xTF32 hi/lo split
-    const int ct = threadIdx.x - 64;
-    int j = 0;
-    for (long long t = blockIdx.x; t < args.n_tiles; t += gridDim.x, ++j) {
-      tc::mbar_wait(full, j & 1);
-      tc::tf32_split_tile<SPLIT>(smem, smem + tma_bytes, (int)(tma_bytes / 4), ct, 32 * CONV_WARPS);
-      tc::fence_proxy_async_smem();
-      __syncwarp();
-      if (lane == 0) tc::mbar_arrive(conv);
+  } else if (warp >= CONV0 && warp < EPI0) {
+    // ---- operand rounding (TF32 round-to-nearest) or 3xTF32 hi/lo split of
+    // the operands that did not arrive pre-split
+    const int ct = threadIdx.x - 32 * CONV0;
+    int g = 0;
+    for (long long t = blockIdx.x; t < args.n_tiles; t += gridDim.x) {
+      for (int kb = 0; kb < args.nkb; ++kb, ++g) {
+        const int s = g % S_;
+        tc::mbar_wait(&full[s], (g / S_) & 1);
+        uint8_t* st = smem + s * STAGE;
+        if (!args.a_pre) tc::tf32_split_tile<SPLIT>(st, st + HI, (int)(A_B / 4), ct, 32 * CONV_WARPS);
+        if (!args.b_pre) tc::tf32_split_tile<SPLIT>(st + A_B, st + HI + A_B, (int)(B_B / 4), ct, 32 * CONV_WARPS);
+        tc::fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(&conv[s]);
+      }
     }
   } else if (warp >= EPI0) {
     // ---- epilogue: TMEM -> registers, blend with X_old, write X_new, reduce
@@ -181,15 +215,16 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int row = 32 * quad + lane;
     int j = 0;
     for (long long t = blockIdx.x; t < args.n_tiles; t += gridDim.x, ++j) {
-      const int s = j & 1;
-      tc::mbar_wait(&tfull[s], (j >> 1) & 1);
+      const int acc = j & 1;
+      tc::mbar_wait(&tfull[acc], (j >> 1) & 1);
       tc::fence_after_sync();
       const long long gr = (t % args.n_rb) * 128 + row;
       const long long cb = (t / args.n_rb) * N + part * CW;
       const bool row_ok = gr < args.rows;
       const long long rowbase = args.rows_are_p ? (gr % args.P) + args.PI * (gr / args.P) : gr;
       const long long colstride = args.rows_are_p ? args.P : args.I;
-      const uint32_t taddr = tmem + s * N + ((uint32_t)(32 * quad) << 16) + part * CW;
+      const uint32_t taddr = tmem + acc * N + ((uint32_t)(32 * quad) << 16) + part * CW;
+      float f_d = 0.f, f_b = 0.f, f_c = 0.f, f_n = 0.f;  // per-tile partials (fp32), folded into fp64
 #pragma unroll 1
       for (int c0 = 0; c0 < CW; c0 += 8) {
         uint32_t r[8];
@@ -199,7 +234,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                      : "r"(taddr + c0));
         float x[8];
         uint32_t mw[8];
-        long long off0 = rowbase + colstride * (cb + c0);
+        const long long off0 = rowbase + colstride * (cb + c0);
         const long long rem = args.cols - (cb + c0);
         const int nc = rem < 8 ? (int)rem : 8;
 #pragma unroll
@@ -216,8 +251,8 @@ __global__ void __launch_bounds__(THREADS, 1)
           const long long off = off0 + colstride * q;
           const float c = __uint_as_float(r[q]);
           if (args.objective_only) {
-            const double d = (double)x[q] - (double)c;
-            s_c += d * d;
+            const float d = x[q] - c;
+            f_c += d * d;
           } else {
             float xn;
             if ((mw[q] >> (off & 31)) & 1u) {
@@ -228,18 +263,21 @@ __global__ void __launch_bounds__(THREADS, 1)
               xn = tt / args.onep;
             }
             __stcs(args.Xn + off, xn);
-            const double dx = (double)xn - (double)x[q];
-            const double dc = (double)xn - (double)c;
-            s_d += dx * dx;
-            s_b += (double)x[q] * (double)x[q];
-            s_c += dc * dc;
-            s_n += (double)xn * (double)xn;
+            const float dx = xn - x[q], dc = xn - c;
+            f_d += dx * dx;
+            f_b += x[q] * x[q];
+            f_c += dc * dc;
+            f_n += xn * xn;
           }
         }
       }
+      s_d += (double)f_d;
+      s_b += (double)f_b;
+      s_c += (double)f_c;
+      s_n += (double)f_n;
       tc::fence_before_sync();
       __syncwarp();
-      if (lane == 0) tc::mbar_arrive(&tempty[s]);
+      if (lane == 0) tc::mbar_arrive(&tempty[acc]);
     }
   }
   // fixed-order reduction: warp shuffle tree, then warps in index order
@@ -267,20 +305,23 @@ __global__ void __launch_bounds__(THREADS, 1)
 }
 
 template <int N, bool SPLIT>
-int go2(const CUtensorMap& ma, const CUtensorMap& mb, const ComposeArgs& a, int grid, cudaStream_t st) {
-  const int smem = (128 + N) * a.kp * 4 * (SPLIT ? 2 : 1) + 1024 + 256;
+int go2(const CUtensorMap* maps, ComposeArgs a, int grid, cudaStream_t st) {
+  constexpr int STAGE = (128 + N) * KB * 4 * (SPLIT ? 2 : 1);
+  a.stages = std::min(4, (200 * 1024) / STAGE);
+  if (a.stages < 1) throw std::runtime_error("compose_tc: tile does not fit in shared memory");
+  const int smem = a.stages * STAGE + 1024 + 256;
   auto fn = k_compose_tc<N, SPLIT>;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) throw std::runtime_error(std::string("compose_tc smem: ") + cudaGetErrorString(e));
-  fn<<<grid, THREADS, smem, st>>>(ma, mb, a);
+  fn<<<grid, THREADS, smem, st>>>(maps[0], maps[1], maps[2], maps[3], a);
   e = cudaGetLastError();
   if (e != cudaSuccess) throw std::runtime_error(std::string("compose_tc: ") + cudaGetErrorString(e));
   return grid;
 }
 
 template <int N>
-int go(const CUtensorMap& ma, const CUtensorMap& mb, const ComposeArgs& a, int grid, bool split3, cudaStream_t st) {
-  return split3 ? go2<N, true>(ma, mb, a, grid, st) : go2<N, false>(ma, mb, a, grid, st);
+int go(const CUtensorMap* maps, const ComposeArgs& a, int grid, bool split3, cudaStream_t st) {
+  return split3 ? go2<N, true>(maps, a, grid, st) : go2<N, false>(maps, a, grid, st);
 }
 
 }  // namespace
@@ -293,8 +334,8 @@ bool tc_compose_supported(int64_t I, int64_t P, int64_t p, int64_t S) {
   return true;
 }
 
-int launch_compose_tc(const float* A, const float* M, const float* Xo, const uint32_t* maskbits, float* Xn,
-                      int64_t I, int64_t P, int64_t S, int64_t p, double rho, bool objective_only, double* partials,
+int launch_compose_tc(const ComposeOperands& op, const float* Xo, const uint32_t* maskbits, float* Xn, int64_t I,
+                      int64_t P, int64_t S, int64_t p, double rho, bool objective_only, double* partials,
                       int64_t partial_cap, int n_sm, bool split3, cudaStream_t st) {
   ComposeArgs a;
   a.Xo = Xo;
@@ -304,7 +345,7 @@ int launch_compose_tc(const float* A, const float* M, const float* Xo, const uin
   a.P = P;
   a.PI = P * I;
   a.I = I;
-  a.kp = (int)((S + 7) / 8 * 8);
+  a.nkb = (int)((S + KB - 1) / KB);
   a.rows_are_p = P > 1;
   a.rho = (float)rho;
   a.onep = (float)(1.0 + rho);
@@ -316,8 +357,6 @@ int launch_compose_tc(const float* A, const float* M, const float* Xo, const uin
     N = (int)((I + 31) / 32 * 32);
     if (N > 256) N = 256;
   }
-  while (N > 32 && (128 + N) * a.kp * 4 * (split3 ? 2 : 1) + 1280 > 200 * 1024) N /= 2;
-  if (N != 32 && N != 64 && N != 96 && N != 128 && N != 160 && N != 192 && N != 224 && N != 256) N = 256;
   a.n_rb = (a.rows + 127) / 128;
   // a tile's 128 rows are one contiguous run of X when rows = i, or rows = p
   // within one run of the fastest modes (P a multiple of 128)
@@ -326,24 +365,55 @@ int launch_compose_tc(const float* A, const float* M, const float* Xo, const uin
   a.n_tiles = a.n_rb * n_cb;
   int grid = (int)std::min<long long>(a.n_tiles, n_sm);
   if (grid > partial_cap) throw std::runtime_error("compose partial buffer too small");
-  // operand maps: rows operand (A) and cols operand (B), both [extent, S] 32-bit MN-major
+  // the rows operand and the cols operand, each [extent, S] 32-bit MN-major;
+  // "pre" tensors: hi = rn_tf32(x), lo = x - hi already in HBM
+  const float* Mh = op.m_hi ? op.m_hi : op.m;
+  const float* Ah = op.a_hi ? op.a_hi : op.a;
   uint64_t dm[2] = {(uint64_t)p, (uint64_t)S}, sm_[1] = {(uint64_t)p * 4};
   uint64_t da[2] = {(uint64_t)I, (uint64_t)S}, sa[1] = {(uint64_t)I * 4};
-  uint32_t box[2] = {32, (uint32_t)a.kp};
-  CUtensorMap mM = tc_make_map_f32(M, 2, dm, sm_, box, true);
-  CUtensorMap mA = tc_make_map_f32(A, 2, da, sa, box, true);
-  const CUtensorMap& rowsmap = a.rows_are_p ? mM : mA;
-  const CUtensorMap& colsmap = a.rows_are_p ? mA : mM;
-  switch (N) {
-    case 32: return go<32>(rowsmap, colsmap, a, grid, split3, st);
-    case 64: return go<64>(rowsmap, colsmap, a, grid, split3, st);
-    case 96: return go<96>(rowsmap, colsmap, a, grid, split3, st);
-    case 128: return go<128>(rowsmap, colsmap, a, grid, split3, st);
-    case 160: return go<160>(rowsmap, colsmap, a, grid, split3, st);
-    case 192: return go<192>(rowsmap, colsmap, a, grid, split3, st);
-    case 224: return go<224>(rowsmap, colsmap, a, grid, split3, st);
-    default: return go<256>(rowsmap, colsmap, a, grid, split3, st);
+  uint32_t box[2] = {32, KB};
+  CUtensorMap mM = tc_make_map_f32(Mh, 2, dm, sm_, box, true);
+  CUtensorMap mMl = op.m_lo ? tc_make_map_f32(op.m_lo, 2, dm, sm_, box, true) : mM;
+  CUtensorMap mA = tc_make_map_f32(Ah, 2, da, sa, box, true);
+  CUtensorMap mAl = op.a_lo ? tc_make_map_f32(op.a_lo, 2, da, sa, box, true) : mA;
+  const bool m_pre = op.m_hi != nullptr && (op.m_lo != nullptr || !split3);
+  const bool a_pre = op.a_hi != nullptr && (op.a_lo != nullptr || !split3);
+  CUtensorMap maps[4];
+  if (a.rows_are_p) {
+    maps[0] = mM; maps[1] = mMl; maps[2] = mA; maps[3] = mAl;
+    a.a_pre = m_pre; a.b_pre = a_pre;
+  } else {
+    maps[0] = mA; maps[1] = mAl; maps[2] = mM; maps[3] = mMl;
+    a.a_pre = a_pre; a.b_pre = m_pre;
   }
+  switch (N) {
+    case 32: return go<32>(maps, a, grid, split3, st);
+    case 64: return go<64>(maps, a, grid, split3, st);
+    case 96: return go<96>(maps, a, grid, split3, st);
+    case 128: return go<128>(maps, a, grid, split3, st);
+    case 160: return go<160>(maps, a, grid, split3, st);
+    case 192: return go<192>(maps, a, grid, split3, st);
+    case 224: return go<224>(maps, a, grid, split3, st);
+    default: return go<256>(maps, a, grid, split3, st);
+  }
+}
+
+// hi = rn_tf32(x), lo = x - hi (lo may be null: round only)
+__global__ void k_tf32_split(const float* __restrict__ x, float* __restrict__ hi, float* __restrict__ lo, int64_t n) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+    const float v = x[e];
+    const float h = tc::tf32_rn(v);
+    hi[e] = h;
+    if (lo) lo[e] = v - h;
+  }
+}
+
+void launch_tf32_split(const float* x, float* hi, float* lo, int64_t n, cudaStream_t st) {
+  if (n <= 0) return;
+  int64_t blocks = std::min<int64_t>((n + 255) / 256, 148 * 16);
+  k_tf32_split<<<(unsigned)blocks, 256, 0, st>>>(x, hi, lo, n);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) throw std::runtime_error(std::string("tf32_split: ") + cudaGetErrorString(e));
 }
 
 // 1 bit per entry, F order: bits[w] bit b <-> mask[32 w + b]

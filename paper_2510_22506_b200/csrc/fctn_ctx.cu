@@ -89,6 +89,8 @@ class Ctx : public Executor {
   bool uploaded = false;
   // N = 3 schedule (see compute_z0): Z_0 = X x_0 A_(0) and its A_0 version
   void* Zbuf = nullptr;
+  void* presplit = nullptr;     // fp32 [A hi | A lo | M hi | M lo] for the TC compose
+  int64_t presplit_m_cap = 0;   // largest M_k (entries) that is pre-split
   int64_t z_version = -1;
   int mbuf_holds = -1;   // mode whose M_k currently sits in Mbuf (-1: none)
   bool zroute = true;    // FCTN_NO_ZROUTE=1 disables
@@ -289,10 +291,12 @@ class Ctx : public Executor {
     }
     A64.clear();
     Ac.clear();
-    for (auto* p : {Ascratch, (double*)Mbuf, (double*)Zbuf, Y, G, Fr, Fi, ypart, partials, epart, colstats, gnet[0],
+    for (auto* p : {Ascratch, (double*)Mbuf, (double*)Zbuf, (double*)presplit, Y, G, Fr, Fi, ypart, partials, epart, colstats, gnet[0],
                      gnet[1]})
       cudaFree(p);
     Zbuf = nullptr;
+    presplit = nullptr;
+    presplit_m_cap = 0;
     for (auto* p : E64) cudaFree(p);
     E64.clear();
     Ascratch = nullptr;
@@ -382,6 +386,10 @@ class Ctx : public Executor {
     }
     CK(cudaMalloc(&Ascratch, max_is * sizeof(double)));
     CK(cudaMalloc(&Mbuf, max_m * esize));
+    if (dtype == FCTN_F32) {
+      presplit_m_cap = std::min<int64_t>(max_m, T / 4);
+      CK(cudaMalloc(&presplit, (2 * max_is + 2 * presplit_m_cap) * sizeof(float)));
+    }
     if (n == 3) CK(cudaMalloc(&Zbuf, std::max<int64_t>(1, sh.s_of(0) * (T / sh.dims[0])) * esize));
     z_version = -1;
     mbuf_holds = -1;
@@ -738,9 +746,29 @@ class Ctx : public Executor {
     for (int j = 0; j < k; ++j) P *= sh.dims[j];
     int nb;
     int pm = pbegin(FCTN_K_COMPOSE);
-    if (dtype == FCTN_F32 && use_tc && tc_compose_supported(I, P, p, S))
-      nb = launch_compose_tc((const float*)Ac[k], (const float*)Mbuf, (const float*)X[cur], maskbits,
-                             (float*)X[cur ^ 1], I, P, S, p, rho, objective_only, partials, partial_cap, n_sm, split3, st);
+    if (dtype == FCTN_F32 && use_tc && tc_compose_supported(I, P, p, S)) {
+      // pre-split the small operands in HBM (A_(k) always; M_k when it is at
+      // most a quarter of X) so the kernel converts only what streams
+      ComposeOperands op;
+      op.a = (const float*)Ac[k];
+      op.m = (const float*)Mbuf;
+      float* ah = (float*)presplit;
+      float* al = split3 ? ah + I * S : nullptr;
+      launch_tf32_split(op.a, ah, al, I * S, st);
+      op.a_hi = ah;
+      op.a_lo = al;
+      if (S * p <= presplit_m_cap) {
+        float* mh = ah + 2 * I * S;
+        float* ml = split3 ? mh + S * p : nullptr;
+        launch_tf32_split(op.m, mh, ml, S * p, st);
+        op.m_hi = mh;
+        op.m_lo = ml;
+        ++launches;
+      }
+      ++launches;
+      nb = launch_compose_tc(op, (const float*)X[cur], maskbits, (float*)X[cur ^ 1], I, P, S, p, rho, objective_only,
+                             partials, partial_cap, n_sm, split3, st);
+    }
     else if (dtype == FCTN_F64)
       nb = launch_compose<double>((const double*)Ac[k], (const double*)Mbuf, (const double*)X[cur], mask,
                                   (double*)X[cur ^ 1], I, P, S, p, rho, objective_only, partials, partial_cap, st);

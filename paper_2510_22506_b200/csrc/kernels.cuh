@@ -111,9 +111,18 @@ int launch_compose(const T* A, const T* M, const T* Xold, const uint8_t* mask, T
                    int64_t partial_cap, cudaStream_t st);
 // tcgen05 TF32 path (compose_tc.cu); returns the number of partial rows written
 bool tc_compose_supported(int64_t I, int64_t P, int64_t p, int64_t S);
-int launch_compose_tc(const float* A, const float* M, const float* Xo, const uint32_t* maskbits, float* Xn,
-                      int64_t I, int64_t P, int64_t S, int64_t p, double rho, bool objective_only, double* partials,
+// operands: A_(k) [I, S] and M_k [p, S] fp32; optional pre-split copies
+// (hi = rn_tf32, lo = rest) skip the in-kernel conversion of that operand
+struct ComposeOperands {
+  const float* a = nullptr;
+  const float* m = nullptr;
+  const float *a_hi = nullptr, *a_lo = nullptr, *m_hi = nullptr, *m_lo = nullptr;
+};
+int launch_compose_tc(const ComposeOperands& op, const float* Xo, const uint32_t* maskbits, float* Xn, int64_t I,
+                      int64_t P, int64_t S, int64_t p, double rho, bool objective_only, double* partials,
                       int64_t partial_cap, int n_sm, bool split3, cudaStream_t st);
+// hi = rn_tf32(x), lo = x - hi (lo may be null)
+void launch_tf32_split(const float* x, float* hi, float* lo, int64_t n, cudaStream_t st);
 void launch_pack_mask(const uint8_t* mask, int64_t T, uint32_t* bits, cudaStream_t st);
 // fixed-order final reduction of n x 4 partials into out[0..3]
 void launch_reduce4(const double* partials, int64_t n, double* out, cudaStream_t st);
