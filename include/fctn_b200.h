@@ -146,8 +146,10 @@ int fctn_timer(fctn_ctx* ctx, int op, double* ms);
 #define FCTN_K_STREAM_Y 1 /* K2 X_(k) M_k^T */
 #define FCTN_K_GRAM 2     /* K2 M_k M_k^T */
 #define FCTN_K_REDUCE 3   /* split-K reductions */
-#define FCTN_K_SOLVE 4    /* K3 DFT / Cholesky / inverse / stats */
+#define FCTN_K_SOLVE 4    /* K3 per-frequency Cholesky solves */
 #define FCTN_K_COMPOSE 5  /* K4 compose + blend + reductions */
+#define FCTN_K_DFT 6      /* K3 forward / inverse DFT along mode k (+ factor write, stats) */
+#define FCTN_K_FGRAM 7    /* K3 factor Gram E_k = A_(k)^T A_(k) + stats fold */
 #define FCTN_K_COUNT 8
 int fctn_set_profiling(fctn_ctx* ctx, int on);
 int fctn_get_profile(fctn_ctx* ctx, double* ms, int64_t* launches, double* bytes);

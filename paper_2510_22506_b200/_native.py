@@ -27,7 +27,7 @@ EXPORTS = [
     "fctn_sync", "fctn_selftest_stream", "fctn_timer", "fctn_set_profiling", "fctn_get_profile", "fctn_last_error", "fctn_version",
     "fctn_destroy",
 ]
-K_CLASSES = ["merge", "stream_y", "gram", "reduce", "solve", "compose", "k6", "k7"]
+K_CLASSES = ["merge", "stream_y", "gram", "reduce", "chol", "compose", "dft", "fgram"]
 
 _lib = None
 

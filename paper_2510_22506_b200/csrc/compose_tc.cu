@@ -56,7 +56,7 @@ struct ComposeArgs {
   int rows_are_p;
   int prefetch;               // rows of a tile are contiguous in X: bulk-prefetch them to L2
   int a_pre, b_pre;           // operand arrives pre-split (hi and lo tensors) from HBM
-  float rho, onep;
+  float rho, onep, inv_onep;
   int objective_only;
 };
 
@@ -211,7 +211,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int ew = warp - EPI0;
     const int quad = warp & 3;
     const int part = ew >> 2;                  // column quarter of this warp
-    constexpr int CW = N / 4;                  // columns per warp (multiple of 8)
+    constexpr int CW = N / 4;                  // columns per warp (multiple of 16)
     const int row = 32 * quad + lane;
     int j = 0;
     for (long long t = blockIdx.x; t < args.n_tiles; t += gridDim.x, ++j) {
@@ -226,19 +226,21 @@ __global__ void __launch_bounds__(THREADS, 1)
       const uint32_t taddr = tmem + acc * N + ((uint32_t)(32 * quad) << 16) + part * CW;
       float f_d = 0.f, f_b = 0.f, f_c = 0.f, f_n = 0.f;  // per-tile partials (fp32), folded into fp64
 #pragma unroll 1
-      for (int c0 = 0; c0 < CW; c0 += 8) {
-        uint32_t r[8];
-        asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
-                     : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
-                       "=r"(r[7])
-                     : "r"(taddr + c0));
-        float x[8];
-        uint32_t mw[8];
+      for (int c0 = 0; c0 < CW; c0 += 16) {
+        uint32_t r[16];
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
+            "%14, %15}, [%16];"
+            : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+              "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+            : "r"(taddr + c0));
+        float x[16];
+        uint32_t mw[16];
         const long long off0 = rowbase + colstride * (cb + c0);
         const long long rem = args.cols - (cb + c0);
-        const int nc = rem < 8 ? (int)rem : 8;
+        const int nc = rem < 16 ? (int)rem : 16;
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {  // all loads in flight before the TMEM wait
+        for (int q = 0; q < 16; ++q) {  // all loads in flight before the TMEM wait
           const long long off = off0 + colstride * q;
           x[q] = (row_ok && q < nc) ? __ldcs(args.Xo + off) : 0.0f;
           mw[q] = (row_ok && q < nc && !args.objective_only) ? __ldg(args.maskbits + (off >> 5)) : 0u;
@@ -246,7 +248,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
         if (!row_ok) continue;
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
+        for (int q = 0; q < 16; ++q) {
           if (q >= nc) break;
           const long long off = off0 + colstride * q;
           const float c = __uint_as_float(r[q]);
@@ -258,9 +260,9 @@ __global__ void __launch_bounds__(THREADS, 1)
             if ((mw[q] >> (off & 31)) & 1u) {
               xn = x[q];  // observed entries restored bit for bit (solver.py:235-236)
             } else {
-              float tt = x[q] * args.rho;  // (x*rho + c)/(1+rho), solver.py:232-234
-              tt = tt + c;
-              xn = tt / args.onep;
+              // (x*rho + c)/(1+rho) (solver.py:232-234); the fp32 variant
+              // multiplies by the rounded reciprocal (<= 1 ulp)
+              xn = fmaf(x[q], args.rho, c) * args.inv_onep;
             }
             __stcs(args.Xn + off, xn);
             const float dx = xn - x[q], dc = xn - c;
@@ -349,12 +351,13 @@ int launch_compose_tc(const ComposeOperands& op, const float* Xo, const uint32_t
   a.rows_are_p = P > 1;
   a.rho = (float)rho;
   a.onep = (float)(1.0 + rho);
+  a.inv_onep = (float)(1.0 / (1.0 + rho));
   a.objective_only = objective_only ? 1 : 0;
   a.rows = a.rows_are_p ? p : I;
   a.cols = a.rows_are_p ? I : p;
   int N = 256;
   if (a.rows_are_p) {
-    N = (int)((I + 31) / 32 * 32);
+    N = (int)((I + 63) / 64 * 64);  // epilogue warps take N/4 columns in chunks of 16
     if (N > 256) N = 256;
   }
   a.n_rb = (a.rows + 127) / 128;
@@ -387,13 +390,9 @@ int launch_compose_tc(const ComposeOperands& op, const float* Xo, const uint32_t
     a.a_pre = a_pre; a.b_pre = m_pre;
   }
   switch (N) {
-    case 32: return go<32>(maps, a, grid, split3, st);
     case 64: return go<64>(maps, a, grid, split3, st);
-    case 96: return go<96>(maps, a, grid, split3, st);
     case 128: return go<128>(maps, a, grid, split3, st);
-    case 160: return go<160>(maps, a, grid, split3, st);
     case 192: return go<192>(maps, a, grid, split3, st);
-    case 224: return go<224>(maps, a, grid, split3, st);
     default: return go<256>(maps, a, grid, split3, st);
   }
 }

@@ -719,19 +719,25 @@ class Ctx : public Executor {
     planner->meter.proj += 2 * I * p * S;   // sylvester.py:105
     planner->meter.gram += 2 * S * S * p;   // sylvester.py:58
     // K3: DFT along mode k, per-frequency SPD solves, inverse DFT (sylvester.py:108-116)
-    pm = pbegin(FCTN_K_SOLVE);
     const DftPlan& dp = dft[k];
     const double sgn = sign == FCTN_SIGN_PD ? -1.0 : 1.0;
+    pm = pbegin(FCTN_K_DFT);
     launch_dft_fwd(Y, dp, S, cosT[k], sinT[k], Fr, Fi, st);
+    pend(pm, 8.0 * (I * S + 2.0 * dp.H1 * S), 1);
+    pm = pbegin(FCTN_K_SOLVE);
     launch_chol_solve(G, S, dp.H1, mu[k], Fr, Fi, check_mu[k], dstatus, st);
+    pend(pm, 8.0 * (S * S + 4.0 * dp.H1 * S), 1);
+    pm = pbegin(FCTN_K_DFT);
     if (dtype == FCTN_F64)
       launch_dft_inv<double>(Fr, Fi, dp, S, cosT[k], sinT[k], A64[k], Ascratch, nullptr, extrap, alpha, beta,
                              delta[k], sgn, colstats, st);
     else
       launch_dft_inv<float>(Fr, Fi, dp, S, cosT[k], sinT[k], A64[k], Ascratch, (float*)Ac[k], extrap, alpha, beta,
                             delta[k], sgn, colstats, st);
+    pend(pm, 8.0 * (3.0 * I * S + 2.0 * dp.H1 * S), 1);
+    pm = pbegin(FCTN_K_FGRAM);
     launch_factor_gram(Ascratch, I, S, epart, E64[k], colstats, dstats + 3 * k, st);
-    pend(pm, 8.0 * (4.0 * I * S + 2.0 * dp.H1 * S + S * S), 5);
+    pend(pm, 8.0 * (I * S + S * S), 2);
     if (mbuf_holds >= 0 && mbuf_holds != k) mbuf_holds = -1;  // M_j (j != k) contains A_k
     std::swap(A64[k], Ascratch);
     if (dtype == FCTN_F64) Ac[k] = A64[k];
