@@ -224,16 +224,20 @@ def run_ours(args, wl, name):
     ctx.sync()
     clocks.start()
     ctx.timer_start()
+    t_host0 = time.perf_counter()
     launches = 0
     lasts = []
     flops = 0
+    dev_ms = []
     for _ in range(args.steps):
         stats, ct = ctx.sweep(order)
+        dev_ms.append(float(stats[_native.ST_DEVICE_MS]))
         launches += int(ct[_native.CT_LAUNCHES])
         flops += int(ct[_native.CT_FLOPS])
         lasts.append(order[-1])
         order = tuple(int(v) for v in rng.permutation(n))
     ms = ctx.timer_stop()
+    host_ms = (time.perf_counter() - t_host0) * 1e3
     clk = clocks.stop()
     prof = ctx.get_profile()
     ctx.set_profiling(False)
@@ -264,6 +268,8 @@ def run_ours(args, wl, name):
                   "achieved_GBs": round(bst / (ms_step / 1e3) / 1e9, 1),
                   "frac": round(bst / (ms_step / 1e3) / 1e9 / pk["hbm_gbs"], 4),
                   "flops_ref_per_sweep": flops // args.steps}
+    sweep_roof["host_wall_ms_per_step"] = round(host_ms / args.steps, 4)
+    sweep_roof["sweep_event_ms_median"] = round(float(np.median(dev_ms)), 4)
     kernels = {k: {"ms_per_step": round(v["ms"] / args.steps, 4), "launches_per_step": v["launches"] / args.steps,
                    "GBs": round(v["bytes"] / (v["ms"] / 1e3) / 1e9, 1) if v["ms"] > 0 else None}
                for k, v in prof.items()}
