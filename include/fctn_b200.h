@@ -115,13 +115,27 @@ int fctn_sweep(fctn_ctx* ctx, const int32_t* order, int extrap, double alpha, do
 int fctn_plan_sweeps(int n, const int64_t* dims, const int64_t* rank_tri, int algorithm,
                      int64_t cache_budget, int n_sweeps, const int32_t* orders, int64_t* counters);
 
-/* Multi-GPU (one process per GPU, sharded along mode 0): an NCCL unique id
- * (128 bytes) made on rank 0 and shared by the caller, then the communicator.
- * Per factor update the rank-sized partial products are all-reduced
- * (Y_k, G_k for k != 0; Y_0 rows all-gathered), per sweep 4 scalars. */
+/* Multi-GPU (one process per GPU, X and the mask sharded along mode 0,
+ * SURVEY.md 8e): an NCCL unique id (128 bytes) made on rank 0 and shared by
+ * the caller, then the communicator.  Must be called after fctn_create and
+ * before fctn_upload; the slab is the standard partition
+ * [rank*I0/nranks, (rank+1)*I0/nranks) and fctn_upload / fctn_get_x then move
+ * this rank's slab (extents (hi-lo, I1, ...)).  Factors stay replicated.  Per
+ * factor update k != 0 the slab's partial Y_k is all-reduced, for k == 0 the
+ * slab's rows of Y_0 are all-gathered; per sweep the four sums are
+ * all-reduced.  The Gram of M_k needs no exchange (factor Grams are global). */
 int fctn_nccl_unique_id(uint8_t* id128);
 int fctn_set_comm(fctn_ctx* ctx, const uint8_t* id128, int rank, int nranks, int64_t slab_lo,
                   int64_t slab_hi);
+
+/* The same sharding with host-side collectives (used by the tests to run
+ * ranks that share one GPU, exchanging through gloo): allreduce sums n
+ * doubles in place; allgather writes nranks*n doubles, rank order. Return 0
+ * on success. */
+typedef int (*fctn_host_allreduce_fn)(void* user, double* buf, int64_t n);
+typedef int (*fctn_host_allgather_fn)(void* user, const double* send, double* recv, int64_t n);
+int fctn_set_comm_host(fctn_ctx* ctx, fctn_host_allreduce_fn allreduce, fctn_host_allgather_fn allgather,
+                       void* user, int rank, int nranks, int64_t slab_lo, int64_t slab_hi);
 
 /* Kernel self-test (tests only): Y = X_(k) M^T for a mode-k view X of
  * extents [P, I, Q] (first fastest) and a p-fastest M (p = P*Q, S rows),

@@ -5,6 +5,7 @@
 hand-written sm_100a kernels in `libfctn_b200.so` (C ABI: include/fctn_b200.h).
 """
 from .network import FctnFactors, FctnRank, mode_fold, mode_unfold
+from .shard import Shard
 from .solver import IterationRecord, NumericalFailure, Observation, SolverConfig, SolverResult, run
 
 __version__ = "0.1.0"
@@ -15,6 +16,7 @@ __all__ = [
     "IterationRecord",
     "NumericalFailure",
     "Observation",
+    "Shard",
     "SolverConfig",
     "SolverResult",
     "mode_fold",

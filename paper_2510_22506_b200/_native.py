@@ -23,13 +23,27 @@ CT_FLOPS, CT_MK, CT_COMPOSE, CT_HITS, CT_LAUNCHES, CT_COUNT = 0, 1, 2, 3, 4, 8
 
 EXPORTS = [
     "fctn_create", "fctn_upload", "fctn_set_factors", "fctn_set_rank", "fctn_get_factors", "fctn_get_x",
-    "fctn_objective", "fctn_sweep", "fctn_plan_sweeps", "fctn_nccl_unique_id", "fctn_set_comm",
+    "fctn_objective", "fctn_sweep", "fctn_plan_sweeps", "fctn_nccl_unique_id", "fctn_set_comm", "fctn_set_comm_host",
     "fctn_sync", "fctn_selftest_stream", "fctn_timer", "fctn_set_profiling", "fctn_get_profile", "fctn_last_error", "fctn_version",
     "fctn_destroy",
 ]
 K_CLASSES = ["merge", "stream_y", "gram", "reduce", "chol", "compose", "dft", "fgram"]
 
 _lib = None
+
+HOST_ALLREDUCE = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_double), C.c_int64)
+HOST_ALLGATHER = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_double), C.c_int64)
+
+
+def slab_of(I0: int, rank: int, nranks: int):
+    """Standard partition of mode 0 (fctn_set_comm)."""
+    return rank * I0 // nranks, (rank + 1) * I0 // nranks
+
+
+def nccl_unique_id() -> bytes:
+    buf = (C.c_uint8 * 128)()
+    check(lib().fctn_nccl_unique_id(buf))
+    return bytes(buf)
 
 
 class NativeError(RuntimeError):
@@ -60,6 +74,7 @@ def lib():
     L.fctn_plan_sweeps.argtypes = [C.c_int, i64p, i64p, C.c_int, C.c_int64, C.c_int, C.POINTER(C.c_int32), i64p]
     L.fctn_nccl_unique_id.argtypes = [P]
     L.fctn_set_comm.argtypes = [P, P, C.c_int, C.c_int, C.c_int64, C.c_int64]
+    L.fctn_set_comm_host.argtypes = [P, HOST_ALLREDUCE, HOST_ALLGATHER, P, C.c_int, C.c_int, C.c_int64, C.c_int64]
     L.fctn_sync.argtypes = [P]
     L.fctn_selftest_stream.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int64, C.c_int64, C.c_int64, C.c_int64, P, P,
                                        f64p]
@@ -177,6 +192,8 @@ class Context:
             pass
 
     def upload(self, values: np.ndarray, mask: np.ndarray):
+        if tuple(values.shape) != self.dims or tuple(mask.shape) != self.dims:
+            raise ValueError(f"expected a tensor of extents {self.dims} (this rank's slab), got {values.shape}")
         x = np.asfortranarray(values, dtype=self.np_dtype)
         m = np.asfortranarray(mask, dtype=np.uint8)
         self._check(lib().fctn_upload(self.h, x.ctypes.data_as(C.c_void_p), m.ctypes.data_as(C.c_void_p)))
@@ -219,6 +236,43 @@ class Context:
 
     def sync(self):
         self._check(lib().fctn_sync(self.h))
+
+    def set_comm_nccl(self, uid: bytes, rank: int, nranks: int):
+        lo, hi = slab_of(self.dims[0], rank, nranks)
+        buf = (C.c_uint8 * 128).from_buffer_copy(uid)
+        self._check(lib().fctn_set_comm(self.h, buf, rank, nranks, lo, hi))
+        self._set_slab(lo, hi)
+
+    def set_comm_host(self, allreduce, allgather, rank: int, nranks: int):
+        """allreduce(np.ndarray) sums in place across ranks; allgather(send) ->
+        np.ndarray of nranks*len(send) in rank order.  Both on float64."""
+        lo, hi = slab_of(self.dims[0], rank, nranks)
+
+        def _ar(_u, ptr, n):
+            try:
+                a = np.ctypeslib.as_array(ptr, shape=(n,))
+                allreduce(a)
+                return 0
+            except Exception:  # pragma: no cover
+                return 1
+
+        def _ag(_u, sptr, rptr, n):
+            try:
+                snd = np.ctypeslib.as_array(sptr, shape=(n,))
+                rcv = np.ctypeslib.as_array(rptr, shape=(n * nranks,))
+                rcv[:] = allgather(snd.copy())
+                return 0
+            except Exception:  # pragma: no cover
+                return 1
+
+        self._host_cbs = (HOST_ALLREDUCE(_ar), HOST_ALLGATHER(_ag))  # keep alive
+        self._check(lib().fctn_set_comm_host(self.h, self._host_cbs[0], self._host_cbs[1], None, rank, nranks, lo,
+                                             hi))
+        self._set_slab(lo, hi)
+
+    def _set_slab(self, lo, hi):
+        self.slab = (lo, hi)
+        self.dims = (hi - lo,) + self.dims[1:]
 
     def timer_start(self):
         self._check(lib().fctn_timer(self.h, 0, None))

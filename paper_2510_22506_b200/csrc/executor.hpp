@@ -3,6 +3,7 @@
 #pragma once
 
 #include <cstdint>
+#include <vector>
 
 #include "plan.hpp"
 
@@ -11,7 +12,9 @@ namespace fctn {
 class Executor {
  public:
   virtual ~Executor() {}
-  virtual int64_t alloc(int64_t numel) = 0;   // compute-dtype elements
+  // a buffer for a tensor with these labels (extents: the executor's own,
+  // possibly sharded, shape)
+  virtual int64_t alloc_labels(const std::vector<int>& labels) = 0;
   virtual void free(int64_t buf) = 0;
   virtual bool is_fixed_buffer(int64_t buf) const = 0;
   virtual void contract(const ContractOp& op) = 0;

@@ -5,6 +5,8 @@
 // small solve workspaces.  One sweep = one host call; the host sees only the
 // few sweep scalars copied back at the end (solver.py:346-388 needs them).
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
 
 #include <algorithm>
 #include <cmath>
@@ -42,12 +44,50 @@ struct CudaError : std::runtime_error {
 
 static const int64_t M_ID = 0;  // fixed executor id of the M_k buffer
 
+// Collectives of the mode-0 sharded sweep: NCCL on the
+// context stream (resolved at run time from the process's libnccl, so the
+// library has no link-time NCCL dependency and shares torch's copy), or a
+// host callback pair (tests: gloo over host memory, ranks sharing one GPU).
+struct Comm {
+  int kind = 0;  // 0 none, 1 NCCL, 2 host callbacks
+  // NCCL
+  void* nccl = nullptr;
+  ncclResult_t (*allreduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) =
+      nullptr;
+  ncclResult_t (*allgather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*destroy)(ncclComm_t) = nullptr;
+  // host
+  fctn_host_allreduce_fn h_allreduce = nullptr;
+  fctn_host_allgather_fn h_allgather = nullptr;
+  void* user = nullptr;
+  double* hbuf = nullptr;  // pinned staging
+  int64_t hcap = 0;
+};
+
+static void* nccl_lib() {
+  static void* h = nullptr;
+  if (!h) {
+    h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) throw std::runtime_error("libnccl.so.2 not found (needed for multi-GPU sharding)");
+  }
+  return h;
+}
+template <typename F>
+static F nccl_sym(const char* name) {
+  void* p = dlsym(nccl_lib(), name);
+  if (!p) throw std::runtime_error(std::string("NCCL symbol missing: ") + name);
+  return reinterpret_cast<F>(p);
+}
+
 class Ctx : public Executor {
  public:
   int device = 0;
   int dtype = FCTN_F64;
   size_t esize = 8;
-  Shape sh;
+  Shape sh;   // execution shape (mode 0 = this rank's slab)
+  Shape gsh;  // global shape: factors, solves, FLOP meter, reuse-cache budget
   std::vector<double> lam, delta;
   int sign = FCTN_SIGN_PD;
   double rho = 0.1;
@@ -94,6 +134,15 @@ class Ctx : public Executor {
   int64_t z_version = -1;
   int mbuf_holds = -1;   // mode whose M_k currently sits in Mbuf (-1: none)
   bool zroute = true;    // FCTN_NO_ZROUTE=1 disables
+  // mode-0 sharding: rows [slab_lo, slab_hi) of mode 0 live here
+  int rank = 0, nranks = 1;
+  int64_t slab_lo = 0, slab_hi = 0, slab_max = 0;
+  void* Aslab = nullptr;   // rows [slab_lo, slab_hi) of A_(0), compute dtype
+  double* yloc = nullptr;  // this rank's rows of Y_0 (slab_max x s_0)
+  double* gbuf = nullptr;  // all-gathered rows (nranks x slab_max x s_0)
+  Comm comm;
+  bool sharded() const { return nranks > 1 || slab_lo != 0 || slab_hi != gsh.dims[0]; }
+  const void* fac_ptr(int k) const { return (k == 0 && Aslab) ? Aslab : Ac[k]; }
 
   // profiling: events bracketing launch groups, accumulated per class
   struct Mark {
@@ -150,7 +199,9 @@ class Ctx : public Executor {
   ~Ctx() override { release_all(); }
 
   // ------------------------------------------------------------ executor
-  int64_t alloc(int64_t numel) override {
+  int64_t alloc_labels(const std::vector<int>& labels) override {
+    int64_t numel = 1;
+    for (int l : labels) numel *= sh.extent(l);
     void* p = nullptr;
     CK(cudaMallocAsync(&p, std::max<int64_t>(numel, 1) * esize, st));
     int64_t id = next_id++;
@@ -167,7 +218,7 @@ class Ctx : public Executor {
   bool is_fixed_buffer(int64_t id) const override { return id == M_ID; }
 
   void* ptr_of(const LTensor& t) {
-    if (t.factor >= 0) return Ac[t.factor];
+    if (t.factor >= 0) return const_cast<void*>(fac_ptr(t.factor));
     if (t.buf == M_ID) return Mbuf;
     auto it = bufs.find(t.buf);
     if (it == bufs.end()) throw std::runtime_error("unknown buffer id");
@@ -291,10 +342,12 @@ class Ctx : public Executor {
     }
     A64.clear();
     Ac.clear();
-    for (auto* p : {Ascratch, (double*)Mbuf, (double*)Zbuf, (double*)presplit, Y, G, Fr, Fi, ypart, partials, epart, colstats, gnet[0],
-                     gnet[1]})
+    for (auto* p : {Ascratch, (double*)Mbuf, (double*)Zbuf, (double*)presplit, (double*)Aslab, yloc, gbuf, Y, G, Fr,
+                     Fi, ypart, partials, epart, colstats, gnet[0], gnet[1]})
       cudaFree(p);
     Zbuf = nullptr;
+    Aslab = nullptr;
+    yloc = gbuf = nullptr;
     presplit = nullptr;
     presplit_m_cap = 0;
     for (auto* p : E64) cudaFree(p);
@@ -305,6 +358,9 @@ class Ctx : public Executor {
   }
   void release_all() {
     if (st) cudaStreamSynchronize(st);
+    if (comm.kind == 1 && comm.nccl && comm.destroy) comm.destroy((ncclComm_t)comm.nccl);
+    if (comm.hbuf) cudaFreeHost(comm.hbuf);
+    comm = Comm();
     release_shape_buffers();
     for (auto* p : mu) cudaFree(p);
     for (auto* p : cosT) cudaFree(p);
@@ -345,18 +401,20 @@ class Ctx : public Executor {
   }
 
   void configure_shape() {
-    // (re)allocate everything whose size depends on the rank table
+    // (re)allocate everything whose size depends on the rank table; factor,
+    // solve and Gram buffers follow the global shape, X-sized ones the slab
     release_shape_buffers();
     const int n = sh.n;
-    const int64_t T = sh.total();
+    const int64_t T = sh.total();  // local
     int64_t max_is = 1, max_ss = 1, max_m = 1, max_h = 1, max_yp = 1, max_part = 1, max_ep = 1, max_s = 1;
     for (int k = 0; k < n; ++k) {
-      int64_t I = sh.dims[k], S = sh.s_of(k), p = T / I;
-      max_is = std::max(max_is, I * S);
+      const int64_t Ig = gsh.dims[k], S = gsh.s_of(k);
+      const int64_t I = sh.dims[k], p = T / I;
+      max_is = std::max(max_is, Ig * S);
       max_ss = std::max(max_ss, S * S);
       max_s = std::max(max_s, S);
       max_m = std::max(max_m, S * p);
-      max_h = std::max(max_h, (I / 2 + 1) * S);
+      max_h = std::max(max_h, (Ig / 2 + 1) * S);
       StreamPlan sy = plan_stream(I, S, p, target_ctas());
       max_yp = std::max(max_yp, (int64_t)sy.nsplit * I * S);
       if (tc_ok(k)) {
@@ -366,7 +424,7 @@ class Ctx : public Executor {
         max_yp = std::max(max_yp, (tp.nsplit * I * S + 1) / 2);  // float partials in the double buffer
       }
       max_part = std::max(max_part, ((I + 63) / 64) * ((p + 63) / 64));
-      max_ep = std::max(max_ep, (int64_t)fgram_splits(I) * S * S);
+      max_ep = std::max(max_ep, (int64_t)fgram_splits(Ig) * S * S);
     }
     A64.assign(n, nullptr);
     Ac.assign(n, nullptr);
@@ -374,7 +432,7 @@ class Ctx : public Executor {
     for (int k = 0; k < n; ++k) {
       // every fp64 factor slot has the max size: the solve output buffer is
       // swapped with the factor it replaces, so slots migrate between modes
-      int64_t e = sh.dims[k] * sh.s_of(k);
+      int64_t e = gsh.dims[k] * gsh.s_of(k);
       CK(cudaMalloc(&A64[k], max_is * sizeof(double)));
       CK(cudaMemset(A64[k], 0, max_is * sizeof(double)));
       CK(cudaMalloc(&E64[k], max_ss * sizeof(double)));
@@ -383,6 +441,12 @@ class Ctx : public Executor {
       } else {
         Ac[k] = A64[k];
       }
+    }
+    if (sharded()) {
+      const int64_t S0 = gsh.s_of(0);
+      CK(cudaMalloc(&Aslab, std::max<int64_t>(1, slab_max * S0) * esize));
+      CK(cudaMalloc(&yloc, std::max<int64_t>(1, slab_max * S0) * sizeof(double)));
+      CK(cudaMalloc(&gbuf, std::max<int64_t>(1, nranks * slab_max * S0) * sizeof(double)));
     }
     CK(cudaMalloc(&Ascratch, max_is * sizeof(double)));
     CK(cudaMalloc(&Mbuf, max_m * esize));
@@ -401,7 +465,7 @@ class Ctx : public Executor {
     CK(cudaMalloc(&epart, max_ep * sizeof(double)));
     CK(cudaMalloc(&colstats, max_s * 3 * sizeof(double)));
     partial_cap = std::max<int64_t>(max_part, 4 * n_sm);
-    CK(cudaMalloc(&partials, max_part * 4 * sizeof(double)));
+    CK(cudaMalloc(&partials, partial_cap * 4 * sizeof(double)));
     int64_t gcap = max_ss;
     for (int k = 0; k < n; ++k) gcap = std::max(gcap, gram_network_peak(k));
     CK(cudaMalloc(&gnet[0], gcap * sizeof(double)));
@@ -409,8 +473,66 @@ class Ctx : public Executor {
     cscratch_cap = std::max<int64_t>(std::max<int64_t>(1, 4 * gcap), (int64_t)(2 * n_sm + 8) * max_is);
     CK(cudaMalloc(&cscratch, cscratch_cap * sizeof(double)));
     std::vector<int64_t> versions = planner ? planner->versions : std::vector<int64_t>(n, 0);
-    planner.reset(new Planner(sh, budget));
+    planner.reset(new Planner(gsh, budget));  // the reference's chain and budget are global
     planner->versions = versions;
+  }
+
+  // ------------------------------------------------------------ collectives
+  void host_stage(int64_t n) {
+    if (comm.hcap >= n) return;
+    if (comm.hbuf) cudaFreeHost(comm.hbuf);
+    CK(cudaMallocHost(&comm.hbuf, n * sizeof(double)));
+    comm.hcap = n;
+  }
+  void allreduce_sum(double* d, int64_t n) {
+    if (nranks == 1 && comm.kind == 0) return;
+    if (comm.kind == 1) {
+      if (comm.allreduce(d, d, (size_t)n, ncclFloat64, ncclSum, (ncclComm_t)comm.nccl, st) != ncclSuccess)
+        throw std::runtime_error("ncclAllReduce failed");
+    } else if (comm.kind == 2) {
+      host_stage(n);
+      CK(cudaMemcpyAsync(comm.hbuf, d, n * sizeof(double), cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      if (comm.h_allreduce(comm.user, comm.hbuf, n) != 0) throw std::runtime_error("host allreduce callback failed");
+      CK(cudaMemcpyAsync(d, comm.hbuf, n * sizeof(double), cudaMemcpyHostToDevice, st));
+    }
+    ++launches;
+  }
+  void allgather(const double* send, double* recv, int64_t n) {
+    if (comm.kind == 1) {
+      if (comm.allgather(send, recv, (size_t)n, ncclFloat64, (ncclComm_t)comm.nccl, st) != ncclSuccess)
+        throw std::runtime_error("ncclAllGather failed");
+    } else if (comm.kind == 2) {
+      host_stage(n * (nranks + 1));
+      CK(cudaMemcpyAsync(comm.hbuf, send, n * sizeof(double), cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      if (comm.h_allgather(comm.user, comm.hbuf, comm.hbuf + n, n) != 0)
+        throw std::runtime_error("host allgather callback failed");
+      CK(cudaMemcpyAsync(recv, comm.hbuf + n, n * nranks * sizeof(double), cudaMemcpyHostToDevice, st));
+    } else {
+      CK(cudaMemcpyAsync(recv, send, n * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    }
+    ++launches;
+  }
+  // rows [lo, hi) of A_(0) into the slab copy (after every update of A_0)
+  void refresh_slab() {
+    if (!Aslab) return;
+    const int64_t S0 = gsh.s_of(0);
+    launch_copy_rows(A64[0], gsh.dims[0], S0, slab_lo, slab_hi - slab_lo, Aslab, dtype == FCTN_F32, st);
+    ++launches;
+  }
+  // finish Y_k = (sum over ranks of this rank's part) + rho A_prev
+  void finish_y(int k, bool rows_local) {
+    const int64_t Ig = gsh.dims[k], S = gsh.s_of(k);
+    if (rows_local) {  // k == 0: this rank computed its own rows of Y_0 into yloc
+      allgather(yloc, gbuf, slab_max * S);
+      launch_scatter_rows(gbuf, nranks, slab_max, Ig, S, Y, st);
+      ++launches;
+    } else {
+      allreduce_sum(Y, Ig * S);
+    }
+    launch_axpy(Y, A64[k], rho, Ig * S, st);
+    ++launches;
   }
 
   // ------------------------------------------------------------ Gram of M_k
@@ -482,7 +604,7 @@ class Ctx : public Executor {
   // factor statistics (||A - A_prev||^2, ||A||^2, tr A^T L A) and E_k for
   // factor k's current fp64 master (used after fctn_set_factors)
   void factor_refresh(int k) {
-    const int64_t I = sh.dims[k], S = sh.s_of(k);
+    const int64_t I = gsh.dims[k], S = gsh.s_of(k);
     const double sgn = sign == FCTN_SIGN_PD ? -1.0 : 1.0;
     launch_factor_colstats(A64[k], I, S, delta[k], sgn, colstats, st);
     launch_factor_gram(A64[k], I, S, epart, E64[k], colstats, dstats + 3 * k, st);
@@ -504,6 +626,10 @@ class Ctx : public Executor {
       if (d < 1) throw UsageError("extents must be >= 1");
     for (auto t : sh.tri)
       if (t < 1) throw UsageError("rank entries must be >= 1");
+    gsh = sh;
+    slab_lo = 0;
+    slab_hi = sh.dims[0];
+    slab_max = sh.dims[0];
     lam.assign(lm, lm + n);
     delta.assign(dl, dl + n);
     for (int k = 0; k < n; ++k) {
@@ -616,10 +742,10 @@ class Ctx : public Executor {
       TcStreamPlan tp = plan_stream_tc(p0, I0, 1, S0, n_sm, split3);
       tp.kb_per_split = tp.nkb;
       tp.nsplit = 1;
-      launch_stream_tc((const float*)X[cur], (const float*)Ac[0], (float*)Zbuf, p0, I0, 1, S0, tp, st);
+      launch_stream_tc((const float*)X[cur], (const float*)fac_ptr(0), (float*)Zbuf, p0, I0, 1, S0, tp, st);
     } else {
       StreamPlan sp = plan_stream(p0, S0, I0, target_ctas());
-      launch_stream<double>((const double*)X[cur], (const double*)Ac[0], ypart, p0, I0, S0, I0, sp, st);
+      launch_stream<double>((const double*)X[cur], (const double*)fac_ptr(0), ypart, p0, I0, S0, I0, sp, st);
       launch_reduce_splits(ypart, sp.nsplit, p0 * S0, nullptr, 0.0, (double*)Zbuf, st);
       ++launches;
     }
@@ -642,13 +768,14 @@ class Ctx : public Executor {
     if (dtype == FCTN_F32) {
       const float *pa = (const float*)Zbuf, *pb = (const float*)Ac[l];
       launch_contract<float>(sw ? pb : pa, sw ? pa : pb, (float*)ypart, d, (float*)cscratch, 2 * cscratch_cap, n_sm, st);
-      launch_reduce_splits_f32((const float*)ypart, 1, I * S, A64[k], rho, Y, st);
+      launch_reduce_splits_f32((const float*)ypart, 1, I * S, sharded() ? nullptr : A64[k], rho, Y, st);
     } else {
       const double *pa = (const double*)Zbuf, *pb = A64[l];
       launch_contract<double>(sw ? pb : pa, sw ? pa : pb, ypart, d, cscratch, cscratch_cap, n_sm, st);
-      launch_reduce_splits(ypart, 1, I * S, A64[k], rho, Y, st);
+      launch_reduce_splits(ypart, 1, I * S, sharded() ? nullptr : A64[k], rho, Y, st);
     }
     launches += 3;
+    if (sharded()) finish_y(k, false);  // Z_0 summed over this slab only
     pend(pm, (double)esize * (d.rows * d.cols + (sh.total() / sh.dims[0]) * sh.s_of(0)), 3);
   }
   // M_j of the current factors into Mbuf, outside the reference's chain (no meter)
@@ -701,16 +828,21 @@ class Ctx : public Executor {
     }
     pend(pm, (double)esize * (T + S * p), 1);
     pm = pbegin(FCTN_K_REDUCE);
+    // sharded: k == 0 -> this rank's rows of Y_0 (all-gathered), k > 0 ->
+    // this slab's share of Y_k (all-reduced); rho A_prev added after
+    double* yout = (sharded() && k == 0) ? yloc : Y;
+    const double* ap = sharded() ? nullptr : A64[k];
     if (tc)
-      launch_reduce_splits_f32((const float*)ypart, nsplit, I * S, A64[k], rho, Y, st);
+      launch_reduce_splits_f32((const float*)ypart, nsplit, I * S, ap, rho, yout, st);
     else
-      launch_reduce_splits(ypart, nsplit, I * S, A64[k], rho, Y, st);
+      launch_reduce_splits(ypart, nsplit, I * S, ap, rho, yout, st);
     pend(pm, (tc ? 4.0 : 8.0) * nsplit * I * S + 16.0 * I * S, 1);
+    if (sharded()) finish_y(k, k == 0);
   }
 
   void solve_factor(int k, int extrap, double alpha, double beta) {
-    const int64_t T = sh.total();
-    const int64_t I = sh.dims[k], S = sh.s_of(k), p = T / I;
+    const int64_t T = gsh.total();
+    const int64_t I = gsh.dims[k], S = gsh.s_of(k), p = T / I;
     // G_k = M_k M_k^T by the doubled network (sylvester.py:57-59)
     int pm = pbegin(FCTN_K_GRAM);
     int64_t l0 = launches;
@@ -743,6 +875,7 @@ class Ctx : public Executor {
     if (dtype == FCTN_F64) Ac[k] = A64[k];
     launches += 7;
     planner->versions[k] += 1;  // network.py:200
+    if (k == 0) refresh_slab();
   }
 
   void compose(int k, bool objective_only) {
@@ -756,7 +889,7 @@ class Ctx : public Executor {
       // pre-split the small operands in HBM (A_(k) always; M_k when it is at
       // most a quarter of X) so the kernel converts only what streams
       ComposeOperands op;
-      op.a = (const float*)Ac[k];
+      op.a = (const float*)fac_ptr(k);
       op.m = (const float*)Mbuf;
       float* ah = (float*)presplit;
       float* al = split3 ? ah + I * S : nullptr;
@@ -776,12 +909,13 @@ class Ctx : public Executor {
                              partials, partial_cap, n_sm, split3, st);
     }
     else if (dtype == FCTN_F64)
-      nb = launch_compose<double>((const double*)Ac[k], (const double*)Mbuf, (const double*)X[cur], mask,
+      nb = launch_compose<double>((const double*)fac_ptr(k), (const double*)Mbuf, (const double*)X[cur], mask,
                                   (double*)X[cur ^ 1], I, P, S, p, rho, objective_only, partials, partial_cap, st);
     else
-      nb = launch_compose<float>((const float*)Ac[k], (const float*)Mbuf, (const float*)X[cur], mask,
+      nb = launch_compose<float>((const float*)fac_ptr(k), (const float*)Mbuf, (const float*)X[cur], mask,
                                  (float*)X[cur ^ 1], I, P, S, p, rho, objective_only, partials, partial_cap, st);
     launch_reduce4(partials, nb, dstats + 3 * sh.n, st);
+    allreduce_sum(dstats + 3 * sh.n, 4);  // the four sums over all slabs
     launches += 2;
     pend(pm, objective_only ? (double)esize * (S * p + T) : (double)esize * (S * p + 2 * T) + (double)T, 2);
   }
@@ -831,7 +965,7 @@ class Ctx : public Executor {
     }
     int k_last = order.back();
     if (alg == FCTN_ALG_ACCEL) {
-      planner->meter.compose += 2 * (sh.total() / sh.dims[k_last]) * sh.s_of(k_last) * sh.dims[k_last];
+      planner->meter.compose += 2 * (gsh.total() / gsh.dims[k_last]) * gsh.s_of(k_last) * gsh.dims[k_last];
       int kc = k_last;
       if (sh.n == 3 && zroute) {
         // compose through the mode with the smallest M_j (same product, another association)
@@ -968,13 +1102,14 @@ int fctn_upload(fctn_ctx* c, const void* x_F, const uint8_t* mask_F) {
 int fctn_set_factors(fctn_ctx* c, const double* const* a_unf, const int64_t* versions, int reset_cache) {
   return fctn::guarded(&c->impl, [&] {
     Ctx& x = c->impl;
-    for (int k = 0; k < x.sh.n; ++k) {
-      int64_t e = x.sh.dims[k] * x.sh.s_of(k);
+    for (int k = 0; k < x.gsh.n; ++k) {
+      int64_t e = x.gsh.dims[k] * x.gsh.s_of(k);
       CK(cudaMemcpyAsync(x.A64[k], a_unf[k], e * sizeof(double), cudaMemcpyHostToDevice, x.st));
       if (x.dtype == FCTN_F32) fctn::launch_convert_f64_f32(x.A64[k], (float*)x.Ac[k], e, x.st);
       if (versions) x.planner->versions[k] = versions[k];
     }
-    for (int k = 0; k < x.sh.n; ++k) x.factor_refresh(k);
+    for (int k = 0; k < x.gsh.n; ++k) x.factor_refresh(k);
+    x.refresh_slab();
     x.z_version = -1;
     x.mbuf_holds = -1;
     if (reset_cache) x.planner->reset_cache(&x);
@@ -989,6 +1124,7 @@ int fctn_set_rank(fctn_ctx* c, const int64_t* rank_tri) {
     for (int i = 0; i < x.sh.n * (x.sh.n - 1) / 2; ++i)
       if (rank_tri[i] < 1) throw fctn::UsageError("rank entries must be >= 1");
     x.sh.tri.assign(rank_tri, rank_tri + x.sh.n * (x.sh.n - 1) / 2);
+    x.gsh.tri = x.sh.tri;
     x.configure_shape();
   });
 }
@@ -996,8 +1132,8 @@ int fctn_set_rank(fctn_ctx* c, const int64_t* rank_tri) {
 int fctn_get_factors(fctn_ctx* c, double* const* a_unf) {
   return fctn::guarded(&c->impl, [&] {
     Ctx& x = c->impl;
-    for (int k = 0; k < x.sh.n; ++k) {
-      int64_t e = x.sh.dims[k] * x.sh.s_of(k);
+    for (int k = 0; k < x.gsh.n; ++k) {
+      int64_t e = x.gsh.dims[k] * x.gsh.s_of(k);
       CK(cudaMemcpyAsync(a_unf[k], x.A64[k], e * sizeof(double), cudaMemcpyDeviceToHost, x.st));
     }
     CK(cudaStreamSynchronize(x.st));
@@ -1061,17 +1197,75 @@ int fctn_plan_sweeps(int n, const int64_t* dims, const int64_t* rank_tri, int al
 }
 
 int fctn_nccl_unique_id(uint8_t* id128) {
-  (void)id128;
-  fctn::g_err = "multi-GPU communicator not built in this library";
-  return 3;
+  return fctn::guarded(nullptr, [&] {
+    static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+    auto get = fctn::nccl_sym<ncclResult_t (*)(ncclUniqueId*)>("ncclGetUniqueId");
+    ncclUniqueId id;
+    if (get(&id) != ncclSuccess) throw std::runtime_error("ncclGetUniqueId failed");
+    std::memcpy(id128, &id, 128);
+  });
 }
 
+namespace fctn {
+// standard partition of mode 0 over ranks; reshape the context to the slab
+static void shard_to(Ctx& x, int rank, int nranks, int64_t lo, int64_t hi) {
+  if (x.uploaded) throw UsageError("set the communicator before uploading data");
+  if (nranks < 1 || rank < 0 || rank >= nranks) throw UsageError("bad rank / nranks");
+  const int64_t I0 = x.gsh.dims[0];
+  if (lo != rank * I0 / nranks || hi != (rank + 1) * I0 / nranks)
+    throw UsageError("slab must be the standard partition [r*I0/n, (r+1)*I0/n)");
+  if (hi <= lo) throw UsageError("empty slab: more ranks than rows of mode 0");
+  x.rank = rank;
+  x.nranks = nranks;
+  x.slab_lo = lo;
+  x.slab_hi = hi;
+  x.slab_max = (I0 + nranks - 1) / nranks;
+  x.sh.dims[0] = hi - lo;
+  const int64_t T = x.sh.total();
+  cudaFree(x.X[0]);
+  cudaFree(x.X[1]);
+  cudaFree(x.mask);
+  cudaFree(x.maskbits);
+  CK(cudaMalloc(&x.X[0], T * x.esize));
+  CK(cudaMalloc(&x.X[1], T * x.esize));
+  CK(cudaMalloc(&x.mask, T));
+  CK(cudaMalloc(&x.maskbits, ((T + 31) / 32) * sizeof(uint32_t)));
+  x.configure_shape();
+}
+}  // namespace fctn
+
 int fctn_set_comm(fctn_ctx* c, const uint8_t* id128, int rank, int nranks, int64_t slab_lo, int64_t slab_hi) {
-  (void)id128;
-  (void)slab_lo;
-  (void)slab_hi;
   return fctn::guarded(&c->impl, [&] {
-    if (nranks != 1 || rank != 0) throw fctn::UsageError("multi-GPU sharding not available yet");
+    Ctx& x = c->impl;
+    fctn::shard_to(x, rank, nranks, slab_lo, slab_hi);
+    if (nranks > 1 || id128) {
+      using InitFn = ncclResult_t (*)(ncclComm_t*, int, ncclUniqueId, int);
+      auto init = fctn::nccl_sym<InitFn>("ncclCommInitRank");
+      x.comm.allreduce = fctn::nccl_sym<decltype(x.comm.allreduce)>("ncclAllReduce");
+      x.comm.allgather = fctn::nccl_sym<decltype(x.comm.allgather)>("ncclAllGather");
+      x.comm.destroy = fctn::nccl_sym<decltype(x.comm.destroy)>("ncclCommDestroy");
+      ncclUniqueId id;
+      if (!id128) throw fctn::UsageError("an NCCL unique id is required");
+      std::memcpy(&id, id128, 128);
+      ncclComm_t comm;
+      CK(cudaSetDevice(x.device));
+      if (init(&comm, nranks, id, rank) != ncclSuccess) throw std::runtime_error("ncclCommInitRank failed");
+      x.comm.nccl = comm;
+      x.comm.kind = 1;
+    }
+  });
+}
+
+int fctn_set_comm_host(fctn_ctx* c, fctn_host_allreduce_fn allreduce, fctn_host_allgather_fn allgather, void* user,
+                       int rank, int nranks, int64_t slab_lo, int64_t slab_hi) {
+  return fctn::guarded(&c->impl, [&] {
+    Ctx& x = c->impl;
+    if (!allreduce || !allgather) throw fctn::UsageError("both host callbacks are required");
+    fctn::shard_to(x, rank, nranks, slab_lo, slab_hi);
+    x.comm.h_allreduce = allreduce;
+    x.comm.h_allgather = allgather;
+    x.comm.user = user;
+    x.comm.kind = 2;
   });
 }
 

@@ -203,6 +203,64 @@ void launch_permute(const T* in, T* out, const PermDesc& d, int64_t numel, cudaS
 template void launch_permute<double>(const double*, double*, const PermDesc&, int64_t, cudaStream_t);
 template void launch_permute<float>(const float*, float*, const PermDesc&, int64_t, cudaStream_t);
 
+// rows [lo, lo+rows) of a column-major I x S fp64 matrix -> rows x S (T)
+template <typename T>
+__global__ void k_copy_rows(const double* __restrict__ A, int64_t I, int64_t S, int64_t lo, int64_t rows,
+                            T* __restrict__ out) {
+  const int64_t n = rows * S;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e % rows, s = e / rows;
+    out[e] = (T)A[lo + i + I * s];
+  }
+}
+
+void launch_copy_rows(const double* A, int64_t I, int64_t S, int64_t lo, int64_t rows, void* out, bool f32,
+                      cudaStream_t st) {
+  const int64_t n = rows * S;
+  if (n <= 0) return;
+  const unsigned blocks = (unsigned)std::min<int64_t>((n + 255) / 256, 148 * 8);
+  if (f32)
+    k_copy_rows<float><<<blocks, 256, 0, st>>>(A, I, S, lo, rows, (float*)out);
+  else
+    k_copy_rows<double><<<blocks, 256, 0, st>>>(A, I, S, lo, rows, (double*)out);
+  check_launch("copy_rows");
+}
+
+// all-gathered blocks [rank][rows_r x S, ld rows_r] (padded to slab_max*S)
+// -> Y (I x S column-major), rank r owning rows [r*I/n, (r+1)*I/n)
+__global__ void k_scatter_rows(const double* __restrict__ g, int nranks, int64_t slab_max, int64_t I, int64_t S,
+                               double* __restrict__ Y) {
+  const int64_t n = I * S;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e % I, s = e / I;
+    int r = (int)((i * nranks) / I);  // owner: largest r with r*I/n <= i
+    while (r + 1 < nranks && (r + 1) * I / nranks <= i) ++r;
+    while (r > 0 && r * I / nranks > i) --r;
+    const int64_t lo = r * I / nranks, rows = (r + 1) * I / nranks - lo;
+    Y[e] = g[(int64_t)r * slab_max * S + (i - lo) + rows * s];
+  }
+}
+
+void launch_scatter_rows(const double* g, int nranks, int64_t slab_max, int64_t I, int64_t S, double* Y,
+                         cudaStream_t st) {
+  const int64_t n = I * S;
+  const unsigned blocks = (unsigned)std::min<int64_t>((n + 255) / 256, 148 * 8);
+  k_scatter_rows<<<blocks, 256, 0, st>>>(g, nranks, slab_max, I, S, Y);
+  check_launch("scatter_rows");
+}
+
+__global__ void k_axpy(double* __restrict__ y, const double* __restrict__ x, double a, int64_t n) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)
+    y[e] += a * x[e];
+}
+
+void launch_axpy(double* y, const double* x, double a, int64_t n, cudaStream_t st) {
+  if (n <= 0) return;
+  const unsigned blocks = (unsigned)std::min<int64_t>((n + 255) / 256, 148 * 8);
+  k_axpy<<<blocks, 256, 0, st>>>(y, x, a, n);
+  check_launch("axpy");
+}
+
 __global__ void k_convert(const double* __restrict__ in, float* __restrict__ out, int64_t n) {
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)
     out[e] = (float)in[e];

@@ -35,6 +35,12 @@ template <typename T>
 void launch_permute(const T* in, T* out, const PermDesc& d, int64_t numel, cudaStream_t st);
 
 void launch_convert_f64_f32(const double* in, float* out, int64_t n, cudaStream_t st);
+// mode-0 sharding helpers (fctn_set_comm)
+void launch_copy_rows(const double* A, int64_t I, int64_t S, int64_t lo, int64_t rows, void* out, bool f32,
+                      cudaStream_t st);
+void launch_scatter_rows(const double* g, int nranks, int64_t slab_max, int64_t I, int64_t S, double* Y,
+                         cudaStream_t st);
+void launch_axpy(double* y, const double* x, double a, int64_t n, cudaStream_t st);
 
 // ---------------------------------------------------------------- K2 stream
 // part[split][i + I*s] = sum_{p in split} X(i,p) * M[p + p_total*s]

@@ -93,7 +93,7 @@ LTensor Planner::contract(const LTensor& a, const LTensor& b, Executor* exec,
   if (out_buf >= 0) {
     op.out.buf = out_buf;
   } else {
-    op.out.buf = exec ? exec->alloc(op.out.numel(sh_)) : g_dry_ids++;
+    op.out.buf = exec ? exec->alloc_labels(op.out.labels) : g_dry_ids++;
   }
   if (exec) exec->contract(op);
   return op.out;

@@ -178,13 +178,20 @@ def _check_laplacians(dims, deltas, sign):
 class _Device:
     """The device side of one run: a context plus host version stamps."""
 
-    def __init__(self, obs_values, obs_mask, rank: FctnRank, lams, deltas, cfg, dtype, device):
+    def __init__(self, obs_values, obs_mask, rank: FctnRank, lams, deltas, cfg, dtype, device, shard=None):
         self.dims = obs_values.shape
         self.n = len(self.dims)
         dt = {"float64": _native.F64, "float32": _native.F32}[dtype]
         self.ctx = _native.Context(device, dt, self.dims, rank.entries, lams, deltas, _SIGNS[cfg.laplacian_sign],
                                    cfg.rho, _native.ALG_ACCEL if cfg.algorithm == "afctnlr" else _native.ALG_PLAIN,
                                    cfg.cache_budget, numeric_exc=NumericalFailure)
+        self.slab = (0, self.dims[0])
+        if shard is not None and shard.nranks > 1:
+            shard.attach(self.ctx)  # before the upload: the context reshapes to its slab
+            self.slab = self.ctx.slab
+            lo, hi = self.slab
+            obs_values = np.asfortranarray(obs_values[lo:hi])
+            obs_mask = np.asfortranarray(obs_mask[lo:hi])
         self.ctx.upload(obs_values, obs_mask)
 
     def load_factors(self, f: FctnFactors, reset_cache: bool):
@@ -193,7 +200,7 @@ class _Device:
         self.ctx.set_factors(f.unfoldings(), f.versions, reset_cache)
 
     def fetch_factors(self, rank: FctnRank, versions) -> FctnFactors:
-        shapes = [(self.dims[k], rank.bond_product(k)) for k in range(self.n)]
+        shapes = [(self.dims[k], rank.bond_product(k)) for k in range(self.n)]  # global extents
         unf = self.ctx.get_factors(shapes)
         f = FctnFactors([mode_fold(u, k, rank.factor_shape(k, self.dims)) for k, u in enumerate(unf)])
         f.versions = list(versions)
@@ -229,8 +236,13 @@ def _grow_with_continuity(dev: _Device, f: FctnFactors, cap: FctnRank, rng, scal
     return cand, extra
 
 
-def run(obs, cfg: SolverConfig, *, dtype: str = "float64", device: int | None = None) -> SolverResult:
-    """Same contract as `fctnlr.solver.run` (solver.py:277-399)."""
+def run(obs, cfg: SolverConfig, *, dtype: str = "float64", device: int | None = None, shard=None) -> SolverResult:
+    """Same contract as `fctnlr.solver.run` (solver.py:277-399).
+
+    ``shard`` (a `shard.Shard`) runs this call as one rank of a mode-0 sharded
+    sweep: every rank passes the same global observation and config; the
+    returned ``x`` is this rank's slab (``result.slab`` = its rows of mode 0),
+    factors and trace are global and identical on every rank."""
     if not isinstance(obs, Observation):
         obs = Observation(values=obs.values, mask=obs.mask)
     n = obs.values.ndim
@@ -254,7 +266,7 @@ def run(obs, cfg: SolverConfig, *, dtype: str = "float64", device: int | None = 
     order = tuple(range(n))
     accelerated = cfg.algorithm == "afctnlr"
 
-    dev = _Device(obs.values, obs.mask, rank, lams, deltas, cfg, dtype, device)
+    dev = _Device(obs.values, obs.mask, rank, lams, deltas, cfg, dtype, device, shard)
     try:
         dev.load_factors(f, reset_cache=True)
         initial_objective, _ = dev.ctx.objective()
@@ -311,6 +323,7 @@ def run(obs, cfg: SolverConfig, *, dtype: str = "float64", device: int | None = 
                 order = tuple(int(v) for v in rng.permutation(n))  # network.py:515-517
         x = dev.ctx.get_x()
         result.x = np.asfortranarray(x, dtype=np.float64)
+        result.slab = dev.slab
         result.factors = dev.fetch_factors(rank, versions)
         return result
     finally:
