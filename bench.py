@@ -161,8 +161,8 @@ def run_reference(args, wl, name):
     cb["value"] = round(cb["value"], 6)
     line = {"metric": METRIC, "value": cb["value"], "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms / k_done, 3),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": config_of(name, wl, 1),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": config_of(name, wl, ws),
             "cpu_baseline": cb, "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
                                         "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
@@ -172,7 +172,7 @@ def run_reference(args, wl, name):
 def config_of(name, wl, nranks):
     return {"workload": f"{name}: {wl.note}", "dims": list(wl.dims), "rank": wl.rank, "sample_rate": wl.sample_rate,
             "solver": "afctnlr, lam=0.35 delta=0.5 rho=0.1, fixed rank, shuffled orders, seed 0",
-            "parallelism": f"replicas x{nranks}" if nranks > 1 else "single GPU",
+            "parallelism": f"mode-0 sharded over {nranks} GPUs (NCCL)" if nranks > 1 else "single GPU",
             "l2": "inputs larger than the 126 MB L2; no flush" if wl.total * 4 > 126e6 else
                   "working set L2-resident (latency-bound config)"}
 
@@ -208,7 +208,15 @@ def run_ours(args, wl, name):
     obs = P.Observation(truth, mask)
     ctx = _native.Context(local, dt, wl.dims, rk.entries, (0.35,) * n, (0.5,) * n, _native.SIGN_PD, 0.1,
                           _native.ALG_ACCEL, 1 << 30, numeric_exc=P.NumericalFailure)
-    ctx.upload(obs.values, obs.mask)
+    shard = None
+    if ws > 1:
+        # one problem sharded along mode 0, NCCL collectives
+        shard = P.Shard(rank, ws, backend="nccl")
+        shard.attach(ctx)
+        lo, hi = ctx.slab
+        ctx.upload(np.asfortranarray(obs.values[lo:hi]), np.asfortranarray(obs.mask[lo:hi]))
+    else:
+        ctx.upload(obs.values, obs.mask)
     rng = np.random.default_rng(0)
     f = FctnFactors.random(wl.dims, rk, rng)
     ctx.set_factors(f.unfoldings(), f.versions, True)
@@ -249,7 +257,7 @@ def run_ours(args, wl, name):
         ms = float(t.item())
     ctx.close()
     ms_step = ms / args.steps
-    value = ws * args.steps / (ms / 1e3)
+    value = args.steps / (ms / 1e3)  # sweeps of the whole tensor per second (sharded over ws GPUs)
 
     # ---- roofline of the dominant kernel class (largest share of the timed region)
     pk = peaks()
@@ -283,7 +291,8 @@ def run_ours(args, wl, name):
     if dist is not None:
         dist.barrier()
     t0 = time.perf_counter()
-    res = P.run(obs, cfg, dtype="float32" if dt == _native.F32 else "float64", device=local)
+    res = P.run(obs, cfg, dtype="float32" if dt == _native.F32 else "float64", device=local,
+                shard=P.Shard(rank, ws, backend="nccl") if ws > 1 else None)
     t_e2e = time.perf_counter() - t0
     if dist is not None:
         import torch
@@ -293,7 +302,7 @@ def run_ours(args, wl, name):
         t_e2e = float(t.item())
     T = wl.total
     fac_bytes = sum(8 * wl.dims[k] * wl.rank ** (n - 1) for k in range(n))
-    e2e = {"value": round(ws * len(res.trace) / t_e2e, 4), "unit": UNIT,
+    e2e = {"value": round(len(res.trace) / t_e2e, 4), "unit": UNIT,
            "h2d_bytes_per_step": int((T * b + T + fac_bytes) / len(res.trace)),
            "d2h_bytes_per_step": int((T * b + fac_bytes) / len(res.trace)),
            "note": "one run(obs, cfg) call: setup + upload + K sweeps + download, bytes amortised per sweep"}
@@ -312,7 +321,7 @@ def emit_line(args, ws, rank, value, ms_step, wl, name, roofline, sweep_roof, ke
     if rank == 0:
         line = {"metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": ws, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": round(ms_step, 4), "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": wl.dtype, "data": "synthetic",
+                "scaling": "strong", "vs_baseline": None, "dtype": wl.dtype, "data": "synthetic",
                 "config": config_of(name, wl, ws), "roofline": roofline, "sweep_roofline": sweep_roof,
                 "kernels": kernels, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk}
         print(json.dumps(line))
