@@ -22,7 +22,6 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
-#include <cstdlib>
 #include <stdexcept>
 #include <string>
 
@@ -56,7 +55,6 @@ struct ComposeArgs {
   int stages;
   int rows_are_p;
   int prefetch;               // rows of a tile are contiguous in X: bulk-prefetch them to L2
-  int pf_lead;                // prefetch distance in tiles of this CTA
   int a_pre, b_pre;           // operand arrives pre-split (hi and lo tensors) from HBM
   float rho, onep, inv_onep;
   int objective_only;
@@ -149,26 +147,18 @@ __global__ void __launch_bounds__(THREADS, 1)
       }
       __syncwarp();
       if (args.prefetch) {
-        // this tile's successor `lead` steps ahead (and, on the first tile,
-        // everything up to it), so the epilogue's X_old reads hit L2
-        const int lead = args.pf_lead;
-        for (int q = (t == blockIdx.x) ? 0 : lead; q <= lead; ++q) {
-          const long long tp = t + (long long)q * gridDim.x;
-          if (tp >= args.n_tiles) break;
-          const long long pr0 = (tp % args.n_rb) * 128, pc0 = (tp / args.n_rb) * N;
-          const long long rbase = args.rows_are_p ? (pr0 % args.P) + args.PI * (pr0 / args.P) : pr0;
-          const long long cstride = args.rows_are_p ? args.P : args.I;
-          const long long nrow = args.rows - pr0 < 128 ? args.rows - pr0 : 128;
-          for (int c = lane; c < N; c += 32) {
-            const long long gc = pc0 + c;
-            if (gc >= args.cols) break;
-            const long long off = rbase + cstride * gc;
-            prefetch_l2(args.Xo + off, (uint32_t)(((nrow * 4) + 15) & ~15LL));
-            if (!args.objective_only)
-              prefetch_l2(reinterpret_cast<const void*>(reinterpret_cast<uintptr_t>(args.maskbits + (off >> 5)) &
-                                                        ~uintptr_t(15)),
-                          32);
-          }
+        const long long rbase = args.rows_are_p ? (r0 % args.P) + args.PI * (r0 / args.P) : r0;
+        const long long cstride = args.rows_are_p ? args.P : args.I;
+        const long long nrow = args.rows - r0 < 128 ? args.rows - r0 : 128;
+        for (int c = lane; c < N; c += 32) {
+          const long long gc = c0 + c;
+          if (gc >= args.cols) break;
+          const long long off = rbase + cstride * gc;
+          prefetch_l2(args.Xo + off, (uint32_t)(((nrow * 4) + 15) & ~15LL));
+          if (!args.objective_only)
+            prefetch_l2(reinterpret_cast<const void*>(reinterpret_cast<uintptr_t>(args.maskbits + (off >> 5)) &
+                                                      ~uintptr_t(15)),
+                        32);
         }
       }
     }
@@ -235,22 +225,6 @@ __global__ void __launch_bounds__(THREADS, 1)
       const long long colstride = args.rows_are_p ? args.P : args.I;
       const uint32_t taddr = tmem + acc * N + ((uint32_t)(32 * quad) << 16) + part * CW;
       float f_d = 0.f, f_b = 0.f, f_c = 0.f, f_n = 0.f;  // per-tile partials (fp32), folded into fp64
-      // software pipeline: the global loads of chunk c+1 are in flight while
-      // chunk c is blended and stored
-      float x[16], xn_[16];
-      uint32_t mw[16], mn_[16];
-      auto load_chunk = [&](int c0, float* xv, uint32_t* mv) {
-        const long long off0 = rowbase + colstride * (cb + c0);
-        const long long rem = args.cols - (cb + c0);
-        const int nc = rem < 16 ? (int)rem : 16;
-#pragma unroll
-        for (int q = 0; q < 16; ++q) {
-          const long long off = off0 + colstride * q;
-          xv[q] = (row_ok && q < nc) ? __ldcs(args.Xo + off) : 0.0f;
-          mv[q] = (row_ok && q < nc && !args.objective_only) ? __ldg(args.maskbits + (off >> 5)) : 0u;
-        }
-      };
-      load_chunk(0, xn_, mn_);
 #pragma unroll 1
       for (int c0 = 0; c0 < CW; c0 += 16) {
         uint32_t r[16];
@@ -260,17 +234,19 @@ __global__ void __launch_bounds__(THREADS, 1)
             : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
               "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
             : "r"(taddr + c0));
-#pragma unroll
-        for (int q = 0; q < 16; ++q) {
-          x[q] = xn_[q];
-          mw[q] = mn_[q];
-        }
-        if (c0 + 16 < CW) load_chunk(c0 + 16, xn_, mn_);
-        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-        if (!row_ok) continue;
+        float x[16];
+        uint32_t mw[16];
         const long long off0 = rowbase + colstride * (cb + c0);
         const long long rem = args.cols - (cb + c0);
         const int nc = rem < 16 ? (int)rem : 16;
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {  // all loads in flight before the TMEM wait
+          const long long off = off0 + colstride * q;
+          x[q] = (row_ok && q < nc) ? __ldcs(args.Xo + off) : 0.0f;
+          mw[q] = (row_ok && q < nc && !args.objective_only) ? __ldg(args.maskbits + (off >> 5)) : 0u;
+        }
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        if (!row_ok) continue;
 #pragma unroll
         for (int q = 0; q < 16; ++q) {
           if (q >= nc) break;
@@ -388,8 +364,6 @@ int launch_compose_tc(const ComposeOperands& op, const float* Xo, const uint32_t
   // a tile's 128 rows are one contiguous run of X when rows = i, or rows = p
   // within one run of the fastest modes (P a multiple of 128)
   a.prefetch = (!a.rows_are_p || P % 128 == 0) ? 1 : 0;
-  a.pf_lead = 1;
-  if (const char* e = getenv("FCTN_PF_LEAD")) a.pf_lead = atoi(e);
   const long long n_cb = (a.cols + N - 1) / N;
   a.n_tiles = a.n_rb * n_cb;
   int grid = (int)std::min<long long>(a.n_tiles, n_sm);
