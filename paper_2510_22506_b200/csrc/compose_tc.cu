@@ -22,6 +22,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <stdexcept>
 #include <string>
 
@@ -32,6 +33,8 @@ namespace fctn {
 
 CUtensorMap tc_make_map_f32(const void* base, int rank, const uint64_t* dims, const uint64_t* strides_bytes,
                             const uint32_t* box, bool mn32);
+CUtensorMap tc_make_map_f32_plain(const void* base, int rank, const uint64_t* dims, const uint64_t* strides_bytes,
+                                  const uint32_t* box);
 
 namespace {
 
@@ -306,6 +309,311 @@ __global__ void __launch_bounds__(THREADS, 1)
   }
 }
 
+// ---------------------------------------------------------------------------
+// TMA-ring variant (X views TMA can describe): the epilogue never touches
+// global memory for X.  A producer warp streams X_old sub-tiles (128 rows x
+// 32 columns, 16 KB) into a ring of shared-memory slots; the epilogue blends
+// each slot in place and one thread TMA-stores it back as X_new, keeping a
+// few bulk groups in flight.  The bulk engines, not registers, hold the bytes
+// in flight.  Operands stream through 16-row K stages.
+constexpr int KB2 = 16;      // K rows per operand stage
+constexpr int XC = 32;       // columns per X sub-tile
+constexpr int XS = 6;        // X ring slots
+constexpr int XKEEP = 3;     // TMA stores allowed in flight
+constexpr int T_CONV0 = 3, T_EPI0 = T_CONV0 + CONV_WARPS, T_NWARPS = T_EPI0 + EPI_WARPS;
+constexpr int T_THREADS = 32 * T_NWARPS;
+constexpr int XBYTES = 128 * XC * 4;
+
+struct ComposeTmaArgs {
+  const uint32_t* maskbits;
+  double* partials;
+  long long rows, cols, n_rb, n_tiles;
+  long long P, PI, I;
+  int nkb;                     // K stages per tile
+  int rows_are_p;
+  int a_pre, b_pre;
+  float rho, inv_onep;
+  int objective_only;
+};
+
+template <int N>
+__device__ __forceinline__ void x_coords(const ComposeTmaArgs& a, long long t, int j, int& c0, int& c1, int& c2) {
+  const long long r0 = (t % a.n_rb) * 128, col = (t / a.n_rb) * N + (long long)j * XC;
+  if (a.rows_are_p) {  // 3-D view (P, I, Q): rows = fastest-mode run, cols = i
+    c0 = (int)(r0 % a.P);
+    c1 = (int)col;
+    c2 = (int)(r0 / a.P);
+  } else {             // 2-D view (I, p): rows = i, cols = p
+    c0 = (int)r0;
+    c1 = (int)col;
+    c2 = 0;
+  }
+}
+
+template <int N, bool SPLIT>
+__global__ void __launch_bounds__(T_THREADS, 1)
+    k_compose_tma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmAl,
+                  const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUtensorMap tmBl,
+                  const __grid_constant__ CUtensorMap tmXo, const __grid_constant__ CUtensorMap tmXn,
+                  const ComposeTmaArgs args) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  constexpr uint32_t A_B = 128u * KB2 * 4u, B_B = (uint32_t)N * KB2 * 4u;
+  constexpr uint32_t HI = A_B + B_B;
+  constexpr uint32_t STAGE = HI * (SPLIT ? 2 : 1);
+  constexpr int OPS = 2;
+  uint8_t* xring = smem + OPS * STAGE;
+  uint64_t* full = reinterpret_cast<uint64_t*>(xring + XS * XBYTES);
+  uint64_t* conv = full + OPS;
+  uint64_t* empty = conv + OPS;
+  uint64_t* tfull = empty + OPS;   // [2]
+  uint64_t* tempty = tfull + 2;    // [2]
+  uint64_t* xfull = tempty + 2;    // [XS]
+  uint64_t* xempty = xfull + XS;   // [XS]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(xempty + XS);
+  __shared__ double red[4][T_NWARPS];
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr int NCOLS = 2 * N <= 32 ? 32 : 2 * N <= 64 ? 64 : 2 * N <= 128 ? 128 : 2 * N <= 256 ? 256 : 512;
+  constexpr int NX = N / XC;  // X sub-tiles per tile
+
+  if (warp == 0 && lane == 0) {
+    tc::tma_prefetch(&tmA);
+    tc::tma_prefetch(&tmB);
+    tc::tma_prefetch(&tmXo);
+    tc::tma_prefetch(&tmXn);
+    for (int s = 0; s < OPS; ++s) {
+      tc::mbar_init(&full[s], 1);
+      tc::mbar_init(&conv[s], CONV_WARPS);
+      tc::mbar_init(&empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      tc::mbar_init(&tfull[s], 1);
+      tc::mbar_init(&tempty[s], EPI_WARPS);
+    }
+    for (int s = 0; s < XS; ++s) {
+      tc::mbar_init(&xfull[s], 1);
+      tc::mbar_init(&xempty[s], 1);
+    }
+    tc::fence_barrier_init();
+  }
+  if (warp == 1) tc::tmem_alloc<NCOLS>(tmem_slot);
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  const uint32_t tmem = *tmem_slot;
+  double s_d = 0.0, s_b = 0.0, s_c = 0.0, s_n = 0.0;
+
+  if (warp == 0 && lane == 0) {
+    // ---- operand producer
+    uint32_t tx = HI;
+    if (SPLIT) tx += (args.a_pre ? A_B : 0) + (args.b_pre ? B_B : 0);
+    int g = 0;
+    for (long long t = blockIdx.x; t < args.n_tiles; t += gridDim.x) {
+      const int r0 = (int)((t % args.n_rb) * 128), c0 = (int)((t / args.n_rb) * N);
+      for (int kb = 0; kb < args.nkb; ++kb, ++g) {
+        const int s = g % OPS;
+        tc::mbar_wait(&empty[s], ((g / OPS) & 1) ^ 1);
+        tc::mbar_expect_tx(&full[s], tx);
+        uint8_t* st = smem + s * STAGE;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) tc::tma_load_2d(st + c * 2048, &tmA, &full[s], r0 + 32 * c, kb * KB2);
+#pragma unroll
+        for (int c = 0; c < N / 32; ++c)
+          tc::tma_load_2d(st + A_B + c * 2048, &tmB, &full[s], c0 + 32 * c, kb * KB2);
+        if (SPLIT && args.a_pre)
+#pragma unroll
+          for (int c = 0; c < 4; ++c) tc::tma_load_2d(st + HI + c * 2048, &tmAl, &full[s], r0 + 32 * c, kb * KB2);
+        if (SPLIT && args.b_pre)
+#pragma unroll
+          for (int c = 0; c < N / 32; ++c)
+            tc::tma_load_2d(st + HI + A_B + c * 2048, &tmBl, &full[s], c0 + 32 * c, kb * KB2);
+      }
+    }
+  } else if (warp == 2 && lane == 0) {
+    // ---- X_old producer: sub-tiles into the ring
+    int g = 0;
+    for (long long t = blockIdx.x; t < args.n_tiles; t += gridDim.x) {
+      for (int j = 0; j < NX; ++j, ++g) {
+        const int s = g % XS;
+        tc::mbar_wait(&xempty[s], ((g / XS) & 1) ^ 1);
+        tc::mbar_expect_tx(&xfull[s], XBYTES);
+        int c0, c1, c2;
+        x_coords<N>(args, t, j, c0, c1, c2);
+        if (args.rows_are_p)
+          tc::tma_load_3d(xring + s * XBYTES, &tmXo, &xfull[s], c0, c1, c2);
+        else
+          tc::tma_load_2d(xring + s * XBYTES, &tmXo, &xfull[s], c0, c1);
+      }
+    }
+  } else if (warp == 1 && lane == 0) {
+    // ---- MMA issuer
+    constexpr uint32_t idesc = tc::idesc_tf32(128, N, true, true);
+    int g = 0, j = 0;
+    for (long long t = blockIdx.x; t < args.n_tiles; t += gridDim.x, ++j) {
+      const int acc = j & 1;
+      tc::mbar_wait(&tempty[acc], ((j >> 1) & 1) ^ 1);
+      for (int kb = 0; kb < args.nkb; ++kb, ++g) {
+        const int s = g % OPS;
+        tc::mbar_wait(&conv[s], (g / OPS) & 1);
+        tc::fence_after_sync();
+        const uint32_t a = tc::smem_u32(smem + s * STAGE), b = a + A_B;
+#pragma unroll
+        for (int kk = 0; kk < KB2 / 8; ++kk) {
+          const uint64_t ad = tc::sdesc(a + kk * 1024, 2048, 512, 1);
+          const uint64_t bd = tc::sdesc(b + kk * 1024, 2048, 512, 1);
+          const uint32_t first = (kb | kk) != 0;
+          if (SPLIT) {
+            tc::mma_tf32(tmem + acc * N, tc::sdesc(a + HI + kk * 1024, 2048, 512, 1), bd, idesc, first);
+            tc::mma_tf32(tmem + acc * N, ad, tc::sdesc(b + HI + kk * 1024, 2048, 512, 1), idesc, 1);
+          }
+          tc::mma_tf32(tmem + acc * N, ad, bd, idesc, SPLIT ? 1u : first);
+        }
+        tc::mma_commit(&empty[s]);
+      }
+      tc::mma_commit(&tfull[acc]);
+    }
+  } else if (warp >= T_CONV0 && warp < T_EPI0) {
+    // ---- operand rounding / 3xTF32 split of operands not pre-split in HBM
+    const int ct = threadIdx.x - 32 * T_CONV0;
+    int g = 0;
+    for (long long t = blockIdx.x; t < args.n_tiles; t += gridDim.x) {
+      for (int kb = 0; kb < args.nkb; ++kb, ++g) {
+        const int s = g % OPS;
+        tc::mbar_wait(&full[s], (g / OPS) & 1);
+        uint8_t* st = smem + s * STAGE;
+        if (!args.a_pre) tc::tf32_split_tile<SPLIT>(st, st + HI, (int)(A_B / 4), ct, 32 * CONV_WARPS);
+        if (!args.b_pre) tc::tf32_split_tile<SPLIT>(st + A_B, st + HI + A_B, (int)(B_B / 4), ct, 32 * CONV_WARPS);
+        tc::fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(&conv[s]);
+      }
+    }
+  } else if (warp >= T_EPI0) {
+    // ---- epilogue: per X sub-tile, warp (quad, part) blends 32 rows x 8 cols
+    const int ew = warp - T_EPI0;
+    const int quad = warp & 3;
+    const int part = ew >> 2;
+    const int row = 32 * quad + lane;
+    const bool leader = (ew == 0 && lane == 0);
+    int g = 0, j = 0;
+    for (long long t = blockIdx.x; t < args.n_tiles; t += gridDim.x, ++j) {
+      const int acc = j & 1;
+      tc::mbar_wait(&tfull[acc], (j >> 1) & 1);
+      tc::fence_after_sync();
+      const long long gr = (t % args.n_rb) * 128 + row;
+      const bool row_ok = gr < args.rows;
+      const long long rowbase = args.rows_are_p ? (gr % args.P) + args.PI * (gr / args.P) : gr;
+      const long long colstride = args.rows_are_p ? args.P : args.I;
+      float f_d = 0.f, f_b = 0.f, f_c = 0.f, f_n = 0.f;
+      for (int xj = 0; xj < NX; ++xj, ++g) {
+        const int s = g % XS;
+        const int col0 = xj * XC + part * 8;                  // column within the tile
+        const long long gc0 = (t / args.n_rb) * N + col0;     // global column
+        uint32_t r[8];
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                     : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+                       "=r"(r[7])
+                     : "r"(tmem + acc * N + ((uint32_t)(32 * quad) << 16) + col0));
+        uint32_t mw[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const long long off = rowbase + colstride * (gc0 + q);
+          mw[q] = (row_ok && gc0 + q < args.cols && !args.objective_only) ? __ldg(args.maskbits + (off >> 5)) : 0u;
+        }
+        tc::mbar_wait(&xfull[s], (g / XS) & 1);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        float* xs = reinterpret_cast<float*>(xring + s * XBYTES);
+        if (row_ok) {
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            if (gc0 + q >= args.cols) break;
+            float* px = xs + (part * 8 + q) * 128 + row;
+            const float x = *px;
+            const float c = __uint_as_float(r[q]);
+            if (args.objective_only) {
+              const float d = x - c;
+              f_c += d * d;
+            } else {
+              const long long off = rowbase + colstride * (gc0 + q);
+              float xn;
+              if ((mw[q] >> (off & 31)) & 1u) {
+                xn = x;  // observed entries restored bit for bit (solver.py:235-236)
+              } else {
+                xn = fmaf(x, args.rho, c) * args.inv_onep;  // solver.py:232-234 (fp32: reciprocal, <= 1 ulp)
+              }
+              *px = xn;
+              const float dx = xn - x, dc = xn - c;
+              f_d += dx * dx;
+              f_b += x * x;
+              f_c += dc * dc;
+              f_n += xn * xn;
+            }
+          }
+        }
+        // all epilogue warps done with this slot -> one thread stores it
+        tc::fence_proxy_async_smem();
+        tc::named_bar(1, 32 * EPI_WARPS);
+        if (leader) {
+          if (!args.objective_only) {
+            int c0, c1, c2;
+            x_coords<N>(args, t, xj, c0, c1, c2);
+            if (args.rows_are_p)
+              tc::tma_store_3d(&tmXn, xs, c0, c1, c2);
+            else
+              tc::tma_store_2d(&tmXn, xs, c0, c1);
+          }
+          tc::bulk_commit();
+          tc::bulk_wait_read<XKEEP>();
+          if (g >= XKEEP) tc::mbar_arrive(&xempty[(g - XKEEP) % XS]);
+        }
+      }
+      s_d += (double)f_d;
+      s_b += (double)f_b;
+      s_c += (double)f_c;
+      s_n += (double)f_n;
+      tc::fence_before_sync();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&tempty[acc]);
+    }
+    if (leader) tc::bulk_wait<0>();  // X_new fully written before exit
+  }
+  s_d = warp_sum(s_d);
+  s_b = warp_sum(s_b);
+  s_c = warp_sum(s_c);
+  s_n = warp_sum(s_n);
+  if (lane == 0) {
+    red[0][warp] = s_d;
+    red[1][warp] = s_b;
+    red[2][warp] = s_c;
+    red[3][warp] = s_n;
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  if (threadIdx.x < 4) {
+    double v = 0.0;
+    for (int q = 0; q < T_NWARPS; ++q) v += red[threadIdx.x][q];
+    args.partials[blockIdx.x * 4 + threadIdx.x] = v;
+  }
+  if (warp == 1) {
+    tc::fence_after_sync();
+    tc::tmem_dealloc<NCOLS>(tmem);
+  }
+}
+
+template <int N, bool SPLIT>
+int go_tma(const CUtensorMap* maps, const ComposeTmaArgs& a, int grid, cudaStream_t st) {
+  constexpr int STAGE = (128 + N) * KB2 * 4 * (SPLIT ? 2 : 1);
+  const int smem = 2 * STAGE + XS * XBYTES + 1024 + 256;
+  auto fn = k_compose_tma<N, SPLIT>;
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) throw std::runtime_error(std::string("compose_tma smem: ") + cudaGetErrorString(e));
+  fn<<<grid, T_THREADS, smem, st>>>(maps[0], maps[1], maps[2], maps[3], maps[4], maps[5], a);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) throw std::runtime_error(std::string("compose_tma: ") + cudaGetErrorString(e));
+  return grid;
+}
+
 template <int N, bool SPLIT>
 int go2(const CUtensorMap* maps, ComposeArgs a, int grid, cudaStream_t st) {
   constexpr int STAGE = (128 + N) * KB * 4 * (SPLIT ? 2 : 1);
@@ -381,13 +689,65 @@ int launch_compose_tc(const ComposeOperands& op, const float* Xo, const uint32_t
   CUtensorMap mAl = op.a_lo ? tc_make_map_f32(op.a_lo, 2, da, sa, box, true) : mA;
   const bool m_pre = op.m_hi != nullptr && (op.m_lo != nullptr || !split3);
   const bool a_pre = op.a_hi != nullptr && (op.a_lo != nullptr || !split3);
-  CUtensorMap maps[4];
+  CUtensorMap maps[6];
   if (a.rows_are_p) {
     maps[0] = mM; maps[1] = mMl; maps[2] = mA; maps[3] = mAl;
     a.a_pre = m_pre; a.b_pre = a_pre;
   } else {
     maps[0] = mA; maps[1] = mAl; maps[2] = mM; maps[3] = mMl;
     a.a_pre = a_pre; a.b_pre = m_pre;
+  }
+  // TMA-ring variant when TMA can describe the X tiles (rows = a contiguous
+  // run of 128): rows = i (P == 1), or rows = p inside runs of P (P % 128 == 0)
+  const bool tma_x = (!a.rows_are_p || P % 128 == 0) && !getenv("FCTN_COMPOSE_DIRECT");
+  if (tma_x) {
+    ComposeTmaArgs t;
+    t.maskbits = maskbits;
+    t.partials = partials;
+    t.rows = a.rows;
+    t.cols = a.cols;
+    t.n_rb = a.n_rb;
+    t.n_tiles = a.n_tiles;
+    t.P = P;
+    t.PI = P * I;
+    t.I = I;
+    t.nkb = (int)((S + KB2 - 1) / KB2);
+    t.rows_are_p = a.rows_are_p;
+    t.a_pre = a.a_pre;
+    t.b_pre = a.b_pre;
+    t.rho = a.rho;
+    t.inv_onep = a.inv_onep;
+    t.objective_only = a.objective_only;
+    uint32_t box16[2] = {32, KB2};
+    // operand maps with 16-row K boxes
+    CUtensorMap tM = tc_make_map_f32(Mh, 2, dm, sm_, box16, true);
+    CUtensorMap tMl = op.m_lo ? tc_make_map_f32(op.m_lo, 2, dm, sm_, box16, true) : tM;
+    CUtensorMap tA = tc_make_map_f32(Ah, 2, da, sa, box16, true);
+    CUtensorMap tAl = op.a_lo ? tc_make_map_f32(op.a_lo, 2, da, sa, box16, true) : tA;
+    if (a.rows_are_p) {
+      maps[0] = tM; maps[1] = tMl; maps[2] = tA; maps[3] = tAl;
+    } else {
+      maps[0] = tA; maps[1] = tAl; maps[2] = tM; maps[3] = tMl;
+    }
+    if (a.rows_are_p) {
+      const uint64_t Q = (uint64_t)(p / P);
+      uint64_t dx[3] = {(uint64_t)P, (uint64_t)I, Q}, sx[2] = {(uint64_t)P * 4, (uint64_t)P * I * 4};
+      uint32_t bx[3] = {128, XC, 1};
+      maps[4] = tc_make_map_f32_plain(Xo, 3, dx, sx, bx);
+      maps[5] = tc_make_map_f32_plain(Xn, 3, dx, sx, bx);
+    } else {
+      uint64_t dx[2] = {(uint64_t)I, (uint64_t)p}, sx[1] = {(uint64_t)I * 4};
+      uint32_t bx[2] = {128, XC};
+      maps[4] = tc_make_map_f32_plain(Xo, 2, dx, sx, bx);
+      maps[5] = tc_make_map_f32_plain(Xn, 2, dx, sx, bx);
+    }
+    if (N % XC != 0) N = (N + XC - 1) / XC * XC;
+    switch (N) {
+      case 64: return split3 ? go_tma<64, true>(maps, t, grid, st) : go_tma<64, false>(maps, t, grid, st);
+      case 128: return split3 ? go_tma<128, true>(maps, t, grid, st) : go_tma<128, false>(maps, t, grid, st);
+      case 192: return split3 ? go_tma<192, true>(maps, t, grid, st) : go_tma<192, false>(maps, t, grid, st);
+      default: return split3 ? go_tma<256, true>(maps, t, grid, st) : go_tma<256, false>(maps, t, grid, st);
+    }
   }
   switch (N) {
     case 64: return go<64>(maps, a, grid, split3, st);

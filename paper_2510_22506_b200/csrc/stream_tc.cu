@@ -229,6 +229,11 @@ CUtensorMap tc_make_map_f32(const void* base, int rank, const uint64_t* dims, co
                   mn32 ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B);
 }
 
+CUtensorMap tc_make_map_f32_plain(const void* base, int rank, const uint64_t* dims, const uint64_t* strides_bytes,
+                                  const uint32_t* box) {
+  return make_map(base, rank, dims, strides_bytes, box, CU_TENSOR_MAP_SWIZZLE_NONE);
+}
+
 bool tc_stream_supported(int64_t I, int64_t P, int64_t Q, int64_t S) {
   if (S > 128) return false;
   if (I > (1LL << 31) || Q > (1LL << 31) || P > (1LL << 31)) return false;
