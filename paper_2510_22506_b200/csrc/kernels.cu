@@ -136,6 +136,123 @@ __global__ void k_contract_reduce(const T* __restrict__ part, int nsplit, const 
   }
 }
 
+// Resident-rows contraction for large outputs with a short side (the merges
+// that write M_k or big partials): the whole row operand (rows x K, rows <=
+// 512) stays in shared memory for the CTA's lifetime, CTAs walk column tiles
+// persistently, lanes run along rows (the operand holding C's fastest label,
+// so stores coalesce) and each thread keeps RPT rows x CPT columns in
+// registers.  Only the streamed column operand is gathered per tile.
+template <typename T, int RPT, int CPT>
+__global__ void __launch_bounds__(256) k_contract_res(const T* __restrict__ A, const T* __restrict__ B,
+                                                      T* __restrict__ C, const ContractDesc d, int64_t n_ctiles) {
+  constexpr int CT = 8 * CPT;  // columns per tile: 8 warps x CPT
+  extern __shared__ __align__(16) unsigned char smraw[];
+  const int K = (int)d.K;
+  const int rows = (int)d.rows;
+  T* As = reinterpret_cast<T*>(smraw);                     // [K][32*RPT]
+  T* Bs = As + (size_t)K * 32 * RPT;                       // [K][CT]
+  int64_t* sRC = reinterpret_cast<int64_t*>(Bs + (size_t)K * CT);  // [32*RPT]
+  int64_t* sKB = sRC + 32 * RPT;                           // [K]
+  int64_t* sCB = sKB + K;                                  // [CT]
+  int64_t* sCC = sCB + CT;                                 // [CT]
+  const int tid = threadIdx.x, lane = tid & 31, wy = tid >> 5;
+  // resident rows: A[r, k] and the output row offsets
+  for (int e = tid; e < K * 32 * RPT; e += 256) {
+    const int k = e / (32 * RPT), r = e % (32 * RPT);
+    T v = T(0);
+    if (r < rows) {
+      int64_t oa, oc, ka, kb;
+      md_offsets(r, d.nr, d.r_ext, d.r_sa, d.r_sc, oa, oc);
+      md_offsets(k, d.nk, d.k_ext, d.k_sa, d.k_sb, ka, kb);
+      v = A[oa + ka];
+    }
+    As[e] = v;
+  }
+  for (int r = tid; r < 32 * RPT; r += 256) {
+    int64_t oa = 0, oc = 0;
+    if (r < rows) md_offsets(r, d.nr, d.r_ext, d.r_sa, d.r_sc, oa, oc);
+    sRC[r] = oc;
+  }
+  for (int k = tid; k < K; k += 256) {
+    int64_t ka, kb;
+    md_offsets(k, d.nk, d.k_ext, d.k_sa, d.k_sb, ka, kb);
+    sKB[k] = kb;
+  }
+  for (int64_t ct = blockIdx.x; ct < n_ctiles; ct += gridDim.x) {
+    const int64_t c0 = ct * CT;
+    __syncthreads();  // previous tile's Bs / sCC readers are done
+    for (int c = tid; c < CT; c += 256) {
+      int64_t ob = -1, oc = 0;
+      if (c0 + c < d.cols) md_offsets(c0 + c, d.nc, d.c_ext, d.c_sb, d.c_sc, ob, oc);
+      sCB[c] = ob;
+      sCC[c] = oc;
+    }
+    __syncthreads();
+    for (int e = tid; e < K * CT; e += 256) {
+      const int k = e / CT, c = e % CT;
+      const int64_t ob = sCB[c];
+      Bs[e] = ob >= 0 ? B[ob + sKB[k]] : T(0);
+    }
+    __syncthreads();
+    T acc[RPT][CPT];
+#pragma unroll
+    for (int i = 0; i < RPT; ++i)
+#pragma unroll
+      for (int j = 0; j < CPT; ++j) acc[i][j] = T(0);
+    for (int k = 0; k < K; ++k) {
+      T a[RPT], b[CPT];
+#pragma unroll
+      for (int i = 0; i < RPT; ++i) a[i] = As[k * 32 * RPT + lane + 32 * i];
+#pragma unroll
+      for (int j = 0; j < CPT; ++j) b[j] = Bs[k * CT + wy * CPT + j];
+#pragma unroll
+      for (int i = 0; i < RPT; ++i)
+#pragma unroll
+        for (int j = 0; j < CPT; ++j) acc[i][j] += a[i] * b[j];
+    }
+#pragma unroll
+    for (int j = 0; j < CPT; ++j) {
+      const int c = wy * CPT + j;
+      if (sCB[c] < 0) continue;
+      const int64_t cc = sCC[c];
+#pragma unroll
+      for (int i = 0; i < RPT; ++i) {
+        const int r = lane + 32 * i;
+        if (r < rows) C[sRC[r] + cc] = acc[i][j];
+      }
+    }
+  }
+}
+
+template <typename T, int RPT, int CPT>
+static bool res_go(const T* A, const T* B, T* C, const ContractDesc& d, int n_sm, cudaStream_t st) {
+  constexpr int CT = 8 * CPT;
+  const size_t smem = (size_t)d.K * (32 * RPT + CT) * sizeof(T) + (32 * RPT + d.K + 2 * CT) * sizeof(int64_t);
+  if (smem > 160 * 1024) return false;
+  auto fn = k_contract_res<T, RPT, CPT>;
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) throw std::runtime_error(std::string("contract_res smem: ") + cudaGetErrorString(e));
+  }
+  const int64_t n_ct = (d.cols + CT - 1) / CT;
+  const int64_t grid = std::min<int64_t>(n_ct, (int64_t)n_sm * 4);
+  fn<<<(unsigned)grid, 256, smem, st>>>(A, B, C, d, n_ct);
+  check_launch("contract_res");
+  return true;
+}
+
+// dispatch for large outputs with a short row side; false = not applicable
+template <typename T>
+static bool contract_resident(const T* A, const T* B, T* C, const ContractDesc& d, int n_sm, cudaStream_t st) {
+  if (d.rows > 512 || d.cols < 4096 || d.K > 1024) return false;
+  const int rpt = (int)((d.rows + 31) / 32);
+  if (rpt <= 1) return res_go<T, 1, 8>(A, B, C, d, n_sm, st);
+  if (rpt <= 2) return res_go<T, 2, 8>(A, B, C, d, n_sm, st);
+  if (rpt <= 4) return res_go<T, 4, 8>(A, B, C, d, n_sm, st);
+  if (rpt <= 8) return res_go<T, 8, 4>(A, B, C, d, n_sm, st);
+  return res_go<T, 16, 2>(A, B, C, d, n_sm, st);
+}
+
 int64_t contract_split_scratch(const ContractDesc& d, int n_sm) {
   const int64_t tiles = ((d.rows + 63) / 64) * ((d.cols + 63) / 64);
   if (tiles >= n_sm || d.K < 256) return 0;
@@ -150,6 +267,7 @@ void launch_contract(const T* A, const T* B, T* C, const ContractDesc& d, T* scr
   const int64_t tr = (d.rows + 63) / 64, tcn = (d.cols + 63) / 64;
   const int64_t tiles = tr * tcn;
   if (tiles <= 0) return;
+  if (contract_resident<T>(A, B, C, d, n_sm, st)) return;
   int64_t ns = 1;
   if (scratch && tiles < n_sm && d.K >= 256) {
     ns = std::min<int64_t>(d.K / 64, (2 * n_sm + tiles - 1) / tiles);
