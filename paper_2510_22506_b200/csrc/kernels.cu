@@ -241,9 +241,85 @@ static bool res_go(const T* A, const T* B, T* C, const ContractDesc& d, int n_sm
   return true;
 }
 
+// Resident-columns variant: the short side is the column operand (<= 256
+// columns) and the long row operand holds C's fastest label.  Each thread
+// owns one streamed row (its K values in registers) and sweeps all resident
+// columns, CB at a time; lanes run along rows, so both the row gathers and
+// the stores coalesce.
+template <typename T, int KMAX, int CB>
+__global__ void __launch_bounds__(256) k_contract_rescol(const T* __restrict__ A, const T* __restrict__ B,
+                                                         T* __restrict__ C, const ContractDesc d) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  const int K = (int)d.K, cols = (int)d.cols;
+  T* Bs = reinterpret_cast<T*>(smraw);                            // [K][cols]
+  int64_t* sCC = reinterpret_cast<int64_t*>(Bs + (size_t)K * cols);  // [cols]
+  int64_t* sKA = sCC + cols;                                      // [K]
+  for (int e = threadIdx.x; e < K * cols; e += blockDim.x) {
+    const int k = e / cols, c = e % cols;
+    int64_t ob, oc, ka, kb;
+    md_offsets(c, d.nc, d.c_ext, d.c_sb, d.c_sc, ob, oc);
+    md_offsets(k, d.nk, d.k_ext, d.k_sa, d.k_sb, ka, kb);
+    Bs[e] = B[ob + kb];
+  }
+  for (int c = threadIdx.x; c < cols; c += blockDim.x) {
+    int64_t ob, oc;
+    md_offsets(c, d.nc, d.c_ext, d.c_sb, d.c_sc, ob, oc);
+    sCC[c] = oc;
+  }
+  for (int k = threadIdx.x; k < K; k += blockDim.x) {
+    int64_t ka, kb;
+    md_offsets(k, d.nk, d.k_ext, d.k_sa, d.k_sb, ka, kb);
+    sKA[k] = ka;
+  }
+  __syncthreads();
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < d.rows;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    int64_t oa, orc;
+    md_offsets(r, d.nr, d.r_ext, d.r_sa, d.r_sc, oa, orc);
+    T a[KMAX];
+#pragma unroll
+    for (int k = 0; k < KMAX; ++k) a[k] = k < K ? A[oa + sKA[k]] : T(0);
+    for (int c0 = 0; c0 < cols; c0 += CB) {
+      T acc[CB];
+#pragma unroll
+      for (int j = 0; j < CB; ++j) acc[j] = T(0);
+#pragma unroll
+      for (int k = 0; k < KMAX; ++k) {
+        if (k >= K) break;
+#pragma unroll
+        for (int j = 0; j < CB; ++j) acc[j] += a[k] * Bs[k * cols + (c0 + j < cols ? c0 + j : 0)];
+      }
+#pragma unroll
+      for (int j = 0; j < CB; ++j)
+        if (c0 + j < cols) C[orc + sCC[c0 + j]] = acc[j];
+    }
+  }
+}
+
+template <typename T, int KMAX>
+static bool rescol_go(const T* A, const T* B, T* C, const ContractDesc& d, int n_sm, cudaStream_t st) {
+  constexpr int CB = 8;
+  const size_t smem = (size_t)d.K * d.cols * sizeof(T) + (d.cols + d.K) * sizeof(int64_t);
+  if (smem > 160 * 1024) return false;
+  auto fn = k_contract_rescol<T, KMAX, CB>;
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) throw std::runtime_error(std::string("contract_rescol smem: ") + cudaGetErrorString(e));
+  }
+  const int64_t grid = std::min<int64_t>((d.rows + 255) / 256, (int64_t)n_sm * 8);
+  fn<<<(unsigned)grid, 256, smem, st>>>(A, B, C, d);
+  check_launch("contract_rescol");
+  return true;
+}
+
 // dispatch for large outputs with a short row side; false = not applicable
 template <typename T>
 static bool contract_resident(const T* A, const T* B, T* C, const ContractDesc& d, int n_sm, cudaStream_t st) {
+  if (d.cols <= 256 && d.rows >= 65536 && d.K <= 32) {  // long rows, short resident columns
+    if (d.K <= 8) return rescol_go<T, 8>(A, B, C, d, n_sm, st);
+    if (d.K <= 16) return rescol_go<T, 16>(A, B, C, d, n_sm, st);
+    return rescol_go<T, 32>(A, B, C, d, n_sm, st);
+  }
   if (d.rows > 512 || d.cols < 4096 || d.K > 1024) return false;
   const int rpt = (int)((d.rows + 31) / 32);
   if (rpt <= 1) return res_go<T, 1, 8>(A, B, C, d, n_sm, st);
