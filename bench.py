@@ -303,8 +303,8 @@ def run_ours(args, wl, name):
     T = wl.total
     fac_bytes = sum(8 * wl.dims[k] * wl.rank ** (n - 1) for k in range(n))
     e2e = {"value": round(len(res.trace) / t_e2e, 4), "unit": UNIT,
-           "h2d_bytes_per_step": int((T * b + T + fac_bytes) / len(res.trace)),
-           "d2h_bytes_per_step": int((T * b + fac_bytes) / len(res.trace)),
+           "h2d_bytes_per_step": int((T * 8 + T + fac_bytes) / len(res.trace)),  # fp64 values + mask bytes
+           "d2h_bytes_per_step": int((T * 8 + fac_bytes) / len(res.trace)),      # fp64 X + factors
            "note": "one run(obs, cfg) call: setup + upload + K sweeps + download, bytes amortised per sweep"}
     del res
 

@@ -79,6 +79,10 @@ int fctn_create(int device, int dtype, int n, const int64_t* dims, const int64_t
  * mask (one byte per entry, 0/1).  Sets X := values. */
 int fctn_upload(fctn_ctx* ctx, const void* x_F, const uint8_t* mask_F);
 
+/* fctn_upload for float64 host data whatever the context dtype (the FP32
+ * variant converts on the device); mask one byte per entry. */
+int fctn_upload_f64(fctn_ctx* ctx, const double* x_F, const uint8_t* mask_F);
+
 /* Replace every factor (mode-k unfoldings, float64) and their version stamps
  * (network.py:193-200; growth re-layout solver.py:365-367 resets the cache). */
 int fctn_set_factors(fctn_ctx* ctx, const double* const* a_unf, const int64_t* versions,
@@ -91,6 +95,7 @@ int fctn_set_rank(fctn_ctx* ctx, const int64_t* rank_tri);
 /* Device -> host. */
 int fctn_get_factors(fctn_ctx* ctx, double* const* a_unf);
 int fctn_get_x(fctn_ctx* ctx, void* x_F);  /* context dtype, like fctn_upload */
+int fctn_get_x_f64(fctn_ctx* ctx, double* x_F);  /* float64 whatever the context dtype */
 
 /* f(X, {A_k}) of solver.py:209-224 for the context's current X and factors
  * (full composition; used for the initial objective solver.py:302 and the

@@ -22,7 +22,7 @@ ST_PENALTY, ST_STEP_FAC, ST_FNORM_MAX, ST_DEVICE_MS, ST_COUNT = 5, 6, 7, 8, 16
 CT_FLOPS, CT_MK, CT_COMPOSE, CT_HITS, CT_LAUNCHES, CT_COUNT = 0, 1, 2, 3, 4, 8
 
 EXPORTS = [
-    "fctn_create", "fctn_upload", "fctn_set_factors", "fctn_set_rank", "fctn_get_factors", "fctn_get_x",
+    "fctn_create", "fctn_upload", "fctn_upload_f64", "fctn_get_x_f64", "fctn_set_factors", "fctn_set_rank", "fctn_get_factors", "fctn_get_x",
     "fctn_objective", "fctn_sweep", "fctn_plan_sweeps", "fctn_nccl_unique_id", "fctn_set_comm", "fctn_set_comm_host",
     "fctn_sync", "fctn_selftest_stream", "fctn_timer", "fctn_set_profiling", "fctn_get_profile", "fctn_last_error", "fctn_version",
     "fctn_destroy",
@@ -65,6 +65,8 @@ def lib():
     L.fctn_create.argtypes = [C.c_int, C.c_int, C.c_int, i64p, i64p, f64p, f64p, C.c_int, C.c_double, C.c_int,
                               C.c_int64, C.POINTER(P)]
     L.fctn_upload.argtypes = [P, P, P]
+    L.fctn_upload_f64.argtypes = [P, P, P]
+    L.fctn_get_x_f64.argtypes = [P, P]
     L.fctn_set_factors.argtypes = [P, C.POINTER(P), i64p, C.c_int]
     L.fctn_set_rank.argtypes = [P, i64p]
     L.fctn_get_factors.argtypes = [P, C.POINTER(P)]
@@ -197,6 +199,21 @@ class Context:
         x = np.asfortranarray(values, dtype=self.np_dtype)
         m = np.asfortranarray(mask, dtype=np.uint8)
         self._check(lib().fctn_upload(self.h, x.ctypes.data_as(C.c_void_p), m.ctypes.data_as(C.c_void_p)))
+
+    def upload_f64(self, values: np.ndarray, mask: np.ndarray):
+        """fp64 values (F order) and a bool/uint8 mask; the fp32 variant converts
+        on the device (no host-side cast pass)."""
+        if tuple(values.shape) != self.dims or tuple(mask.shape) != self.dims:
+            raise ValueError(f"expected a tensor of extents {self.dims} (this rank's slab), got {values.shape}")
+        x = np.asfortranarray(values, dtype=np.float64)
+        m = np.asfortranarray(mask)
+        m = m.view(np.uint8) if m.dtype == np.bool_ else np.asfortranarray(m, dtype=np.uint8)
+        self._check(lib().fctn_upload_f64(self.h, x.ctypes.data_as(C.c_void_p), m.ctypes.data_as(C.c_void_p)))
+
+    def get_x_f64(self) -> np.ndarray:
+        out = np.empty(self.dims, dtype=np.float64, order="F")
+        self._check(lib().fctn_get_x_f64(self.h, out.ctypes.data_as(C.c_void_p)))
+        return out
 
     def set_rank(self, rank_tri):
         r, rp = _i64(rank_tri)

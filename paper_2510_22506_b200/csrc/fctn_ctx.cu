@@ -472,6 +472,18 @@ class Ctx : public Executor {
     CK(cudaMalloc(&gnet[1], gcap * sizeof(double)));
     cscratch_cap = std::max<int64_t>(std::max<int64_t>(1, 4 * gcap), (int64_t)(2 * n_sm + 8) * max_is);
     CK(cudaMalloc(&cscratch, cscratch_cap * sizeof(double)));
+    // Pre-grow the stream-ordered pool that holds the reuse cache and the
+    // chain intermediates (up to the cache budget, as device bytes, plus two
+    // of the largest partials), so no sweep pays for a pool growth.
+    if (n >= 4) {
+      int64_t big = 0;
+      for (int k = 0; k < n; ++k) big = std::max(big, sh.s_of(k) * (T / sh.dims[k]));
+      const int64_t cache_dev = budget / 8 * (int64_t)esize;
+      const int64_t want = std::min<int64_t>(cache_dev + 2 * big * (int64_t)esize, (int64_t)8 << 30);
+      void* warm = nullptr;
+      if (cudaMallocAsync(&warm, want, st) == cudaSuccess) CK(cudaFreeAsync(warm, st));
+      else cudaGetLastError();
+    }
     std::vector<int64_t> versions = planner ? planner->versions : std::vector<int64_t>(n, 0);
     planner.reset(new Planner(gsh, budget));  // the reference's chain and budget are global
     planner->versions = versions;
@@ -1096,6 +1108,54 @@ int fctn_upload(fctn_ctx* c, const void* x_F, const uint8_t* mask_F) {
     x.uploaded = true;
     x.z_version = -1;
     x.mbuf_holds = -1;
+  });
+}
+
+int fctn_upload_f64(fctn_ctx* c, const double* x_F, const uint8_t* mask_F) {
+  return fctn::guarded(&c->impl, [&] {
+    Ctx& x = c->impl;
+    const int64_t T = x.sh.total();
+    if (x.dtype == FCTN_F64) {
+      CK(cudaMemcpyAsync(x.X[0], x_F, T * 8, cudaMemcpyHostToDevice, x.st));
+    } else {  // fp64 host data, fp32 context: convert on the device, in chunks
+      const int64_t chunk = std::min<int64_t>(T, (int64_t)1 << 26);
+      double* tmp = nullptr;
+      CK(cudaMallocAsync((void**)&tmp, chunk * 8, x.st));
+      for (int64_t o = 0; o < T; o += chunk) {
+        const int64_t n = std::min(chunk, T - o);
+        CK(cudaMemcpyAsync(tmp, x_F + o, n * 8, cudaMemcpyHostToDevice, x.st));
+        fctn::launch_convert_f64_f32(tmp, (float*)x.X[0] + o, n, x.st);
+      }
+      CK(cudaFreeAsync(tmp, x.st));
+    }
+    CK(cudaMemcpyAsync(x.mask, mask_F, T, cudaMemcpyHostToDevice, x.st));
+    fctn::launch_pack_mask(x.mask, T, x.maskbits, x.st);
+    CK(cudaStreamSynchronize(x.st));
+    x.cur = 0;
+    x.uploaded = true;
+    x.z_version = -1;
+    x.mbuf_holds = -1;
+  });
+}
+
+int fctn_get_x_f64(fctn_ctx* c, double* x_F) {
+  return fctn::guarded(&c->impl, [&] {
+    Ctx& x = c->impl;
+    const int64_t T = x.sh.total();
+    if (x.dtype == FCTN_F64) {
+      CK(cudaMemcpyAsync(x_F, x.X[x.cur], T * 8, cudaMemcpyDeviceToHost, x.st));
+    } else {
+      const int64_t chunk = std::min<int64_t>(T, (int64_t)1 << 26);
+      double* tmp = nullptr;
+      CK(cudaMallocAsync((void**)&tmp, chunk * 8, x.st));
+      for (int64_t o = 0; o < T; o += chunk) {
+        const int64_t n = std::min(chunk, T - o);
+        fctn::launch_convert_f32_f64((const float*)x.X[x.cur] + o, tmp, n, x.st);
+        CK(cudaMemcpyAsync(x_F + o, tmp, n * 8, cudaMemcpyDeviceToHost, x.st));
+      }
+      CK(cudaFreeAsync(tmp, x.st));
+    }
+    CK(cudaStreamSynchronize(x.st));
   });
 }
 

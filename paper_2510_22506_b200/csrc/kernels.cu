@@ -460,6 +460,19 @@ __global__ void k_convert(const double* __restrict__ in, float* __restrict__ out
     out[e] = (float)in[e];
 }
 
+__global__ void k_convert_up(const float* __restrict__ in, double* __restrict__ out, int64_t n) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)
+    out[e] = (double)in[e];
+}
+
+void launch_convert_f32_f64(const float* in, double* out, int64_t n, cudaStream_t st) {
+  if (n <= 0) return;
+  int64_t blocks = (n + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  k_convert_up<<<(unsigned)blocks, 256, 0, st>>>(in, out, n);
+  check_launch("convert_up");
+}
+
 void launch_convert_f64_f32(const double* in, float* out, int64_t n, cudaStream_t st) {
   if (n <= 0) return;
   int64_t blocks = (n + 255) / 256;

@@ -35,6 +35,7 @@ template <typename T>
 void launch_permute(const T* in, T* out, const PermDesc& d, int64_t numel, cudaStream_t st);
 
 void launch_convert_f64_f32(const double* in, float* out, int64_t n, cudaStream_t st);
+void launch_convert_f32_f64(const float* in, double* out, int64_t n, cudaStream_t st);
 // mode-0 sharding helpers (fctn_set_comm)
 void launch_copy_rows(const double* A, int64_t I, int64_t S, int64_t lo, int64_t rows, void* out, bool f32,
                       cudaStream_t st);

@@ -192,7 +192,7 @@ class _Device:
             lo, hi = self.slab
             obs_values = np.asfortranarray(obs_values[lo:hi])
             obs_mask = np.asfortranarray(obs_mask[lo:hi])
-        self.ctx.upload(obs_values, obs_mask)
+        self.ctx.upload_f64(obs_values, obs_mask)
 
     def load_factors(self, f: FctnFactors, reset_cache: bool):
         if tuple(f.rank.entries) != self.ctx.rank_tri:
@@ -321,8 +321,7 @@ def run(obs, cfg: SolverConfig, *, dtype: str = "float64", device: int | None = 
                 break
             if accelerated and cfg.shuffle:
                 order = tuple(int(v) for v in rng.permutation(n))  # network.py:515-517
-        x = dev.ctx.get_x()
-        result.x = np.asfortranarray(x, dtype=np.float64)
+        result.x = dev.ctx.get_x_f64()
         result.slab = dev.slab
         result.factors = dev.fetch_factors(rank, versions)
         return result
