@@ -35,6 +35,23 @@ HOST_ALLREDUCE = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_double), C.c_int
 HOST_ALLGATHER = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_double), C.c_int64)
 
 
+def _host_empty(dims) -> np.ndarray:
+    """F-order float64 array for a large download: backed by an anonymous
+    mapping advised for transparent huge pages, so first-touch page faults
+    during the device->host copy are ~512x fewer."""
+    n = int(np.prod(dims))
+    nbytes = n * 8
+    if nbytes < (64 << 20):
+        return np.empty(dims, dtype=np.float64, order="F")
+    import mmap
+    buf = mmap.mmap(-1, nbytes, flags=mmap.MAP_PRIVATE | mmap.MAP_ANONYMOUS)
+    try:
+        buf.madvise(mmap.MADV_HUGEPAGE)
+    except (AttributeError, OSError):
+        pass
+    return np.frombuffer(buf, dtype=np.float64, count=n).reshape(dims, order="F")
+
+
 def slab_of(I0: int, rank: int, nranks: int):
     """Standard partition of mode 0 (fctn_set_comm)."""
     return rank * I0 // nranks, (rank + 1) * I0 // nranks
@@ -211,7 +228,7 @@ class Context:
         self._check(lib().fctn_upload_f64(self.h, x.ctypes.data_as(C.c_void_p), m.ctypes.data_as(C.c_void_p)))
 
     def get_x_f64(self) -> np.ndarray:
-        out = np.empty(self.dims, dtype=np.float64, order="F")
+        out = _host_empty(self.dims)
         self._check(lib().fctn_get_x_f64(self.h, out.ctypes.data_as(C.c_void_p)))
         return out
 

@@ -1111,10 +1111,30 @@ int fctn_upload(fctn_ctx* c, const void* x_F, const uint8_t* mask_F) {
   });
 }
 
+namespace fctn {
+// Page-lock a caller buffer for the duration of one large transfer (the
+// pageable path stages through the driver at a fraction of the PCIe/C2C
+// rate).  Falls back to pageable if registration fails.
+struct HostPin {
+  void* p = nullptr;
+  HostPin(const void* ptr, size_t bytes) {
+    if (bytes < ((size_t)64 << 20) || getenv("FCTN_NO_PIN")) return;
+    if (cudaHostRegister(const_cast<void*>(ptr), bytes, cudaHostRegisterDefault) == cudaSuccess)
+      p = const_cast<void*>(ptr);
+    else
+      cudaGetLastError();
+  }
+  ~HostPin() {
+    if (p) cudaHostUnregister(p);
+  }
+};
+}  // namespace fctn
+
 int fctn_upload_f64(fctn_ctx* c, const double* x_F, const uint8_t* mask_F) {
   return fctn::guarded(&c->impl, [&] {
     Ctx& x = c->impl;
     const int64_t T = x.sh.total();
+    fctn::HostPin pin_x(x_F, (size_t)T * 8), pin_m(mask_F, (size_t)T);
     if (x.dtype == FCTN_F64) {
       CK(cudaMemcpyAsync(x.X[0], x_F, T * 8, cudaMemcpyHostToDevice, x.st));
     } else {  // fp64 host data, fp32 context: convert on the device, in chunks
@@ -1142,6 +1162,7 @@ int fctn_get_x_f64(fctn_ctx* c, double* x_F) {
   return fctn::guarded(&c->impl, [&] {
     Ctx& x = c->impl;
     const int64_t T = x.sh.total();
+    fctn::HostPin pin_x(x_F, (size_t)T * 8);
     if (x.dtype == FCTN_F64) {
       CK(cudaMemcpyAsync(x_F, x.X[x.cur], T * 8, cudaMemcpyDeviceToHost, x.st));
     } else {
