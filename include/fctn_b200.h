@@ -150,6 +150,12 @@ int fctn_set_comm_host(fctn_ctx* ctx, fctn_host_allreduce_fn allreduce, fctn_hos
 int fctn_selftest_stream(int device, int dtype, int use_tc, int64_t I, int64_t P, int64_t Q, int64_t S,
                          const void* x, const void* m, double* y);
 
+/* Kernel self-test (tests only): the per-frequency solves of K3,
+ * (G + mu_w I) a_w = F_w for w < H1 (Re and Im right-hand sides, F stored
+ * [w + H1 s]), in place; `reps` timed launches, best ms returned. */
+int fctn_selftest_chol(int device, int64_t S, int64_t H1, const double* G, const double* mu, double* Fr, double* Fi,
+                       int reps, double* ms_per_launch);
+
 /* Sync the context stream. */
 int fctn_sync(fctn_ctx* ctx);
 

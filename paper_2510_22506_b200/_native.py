@@ -24,7 +24,7 @@ CT_FLOPS, CT_MK, CT_COMPOSE, CT_HITS, CT_LAUNCHES, CT_COUNT = 0, 1, 2, 3, 4, 8
 EXPORTS = [
     "fctn_create", "fctn_upload", "fctn_upload_f64", "fctn_get_x_f64", "fctn_set_factors", "fctn_set_rank", "fctn_get_factors", "fctn_get_x",
     "fctn_objective", "fctn_sweep", "fctn_plan_sweeps", "fctn_nccl_unique_id", "fctn_set_comm", "fctn_set_comm_host",
-    "fctn_sync", "fctn_selftest_stream", "fctn_timer", "fctn_set_profiling", "fctn_get_profile", "fctn_last_error", "fctn_version",
+    "fctn_sync", "fctn_selftest_stream", "fctn_selftest_chol", "fctn_timer", "fctn_set_profiling", "fctn_get_profile", "fctn_last_error", "fctn_version",
     "fctn_destroy",
 ]
 K_CLASSES = ["merge", "stream_y", "gram", "reduce", "chol", "compose", "dft", "fgram"]
@@ -95,6 +95,7 @@ def lib():
     L.fctn_set_comm.argtypes = [P, P, C.c_int, C.c_int, C.c_int64, C.c_int64]
     L.fctn_set_comm_host.argtypes = [P, HOST_ALLREDUCE, HOST_ALLGATHER, P, C.c_int, C.c_int, C.c_int64, C.c_int64]
     L.fctn_sync.argtypes = [P]
+    L.fctn_selftest_chol.argtypes = [C.c_int, C.c_int64, C.c_int64, P, P, P, P, C.c_int, f64p]
     L.fctn_selftest_stream.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int64, C.c_int64, C.c_int64, C.c_int64, P, P,
                                        f64p]
     L.fctn_timer.argtypes = [P, C.c_int, f64p]
@@ -166,6 +167,22 @@ def selftest_stream(x, m, k, use_tc=True, device=0):
                                     m.ctypes.data_as(C.c_void_p), y.ctypes.data_as(C.POINTER(C.c_double)))
     check(rc)
     return y
+
+
+def selftest_chol(G, mu, Fr, Fi, reps=1, device=0):
+    """Per-frequency SPD solves (G + mu_w I) a = F_w on the device; returns
+    (Fr_out, Fi_out, best ms per launch).  F arrays are (H1, S)."""
+    G = np.asfortranarray(G, dtype=np.float64)
+    mu = np.ascontiguousarray(mu, dtype=np.float64)
+    H1, S = Fr.shape
+    fr = np.asfortranarray(Fr, dtype=np.float64).copy(order="F")
+    fi = np.asfortranarray(Fi, dtype=np.float64).copy(order="F")
+    ms = C.c_double()
+    rc = lib().fctn_selftest_chol(int(device), S, H1, G.ctypes.data_as(C.c_void_p), mu.ctypes.data_as(C.c_void_p),
+                                  fr.ctypes.data_as(C.c_void_p), fi.ctypes.data_as(C.c_void_p), int(reps),
+                                  C.byref(ms))
+    check(rc)
+    return fr, fi, float(ms.value)
 
 
 class Context:

@@ -1433,6 +1433,55 @@ int fctn_selftest_stream(int device, int dtype, int use_tc, int64_t I, int64_t P
   });
 }
 
+int fctn_selftest_chol(int device, int64_t S, int64_t H1, const double* G, const double* mu, double* Fr,
+                       double* Fi, int reps, double* ms_per_launch) {
+  return fctn::guarded(nullptr, [&] {
+    CK(cudaSetDevice(device));
+    cudaStream_t st;
+    CK(cudaStreamCreate(&st));
+    double *dG, *dmu, *dFr, *dFi, *wFr, *wFi;
+    int* dstat;
+    CK(cudaMalloc(&dG, S * S * 8));
+    CK(cudaMalloc(&dmu, H1 * 8));
+    CK(cudaMalloc(&dFr, H1 * S * 8));
+    CK(cudaMalloc(&dFi, H1 * S * 8));
+    CK(cudaMalloc(&wFr, H1 * S * 8));
+    CK(cudaMalloc(&wFi, H1 * S * 8));
+    CK(cudaMalloc(&dstat, 4));
+    CK(cudaMemset(dstat, 0, 4));
+    CK(cudaMemcpy(dG, G, S * S * 8, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(dmu, mu, H1 * 8, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(dFr, Fr, H1 * S * 8, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(dFi, Fi, H1 * S * 8, cudaMemcpyHostToDevice));
+    cudaEvent_t a, b;
+    CK(cudaEventCreate(&a));
+    CK(cudaEventCreate(&b));
+    float best = 1e30f;
+    for (int r = 0; r < std::max(reps, 1); ++r) {
+      CK(cudaMemcpyAsync(wFr, dFr, H1 * S * 8, cudaMemcpyDeviceToDevice, st));
+      CK(cudaMemcpyAsync(wFi, dFi, H1 * S * 8, cudaMemcpyDeviceToDevice, st));
+      CK(cudaEventRecord(a, st));
+      fctn::launch_chol_solve(dG, S, H1, dmu, wFr, wFi, NAN, dstat, st);
+      CK(cudaEventRecord(b, st));
+      CK(cudaEventSynchronize(b));
+      float ms;
+      CK(cudaEventElapsedTime(&ms, a, b));
+      best = std::min(best, ms);
+    }
+    if (ms_per_launch) *ms_per_launch = best;
+    CK(cudaMemcpy(Fr, wFr, H1 * S * 8, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(Fi, wFi, H1 * S * 8, cudaMemcpyDeviceToHost));
+    int status = 0;
+    CK(cudaMemcpy(&status, dstat, 4, cudaMemcpyDeviceToHost));
+    for (auto* p : {dG, dmu, dFr, dFi, wFr, wFi}) cudaFree(p);
+    cudaFree(dstat);
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    cudaStreamDestroy(st);
+    if (status) throw fctn::NumericError("factorisation failed");
+  });
+}
+
 int fctn_sync(fctn_ctx* c) {
   return fctn::guarded(&c->impl, [&] { CK(cudaStreamSynchronize(c->impl.st)); });
 }

@@ -40,3 +40,18 @@ def test_stream_fp64_matches_numpy(dims, k, S):
     ref = _unfold(x, k) @ m
     y = _native.selftest_stream(x, m, k)
     assert np.linalg.norm(y - ref) / np.linalg.norm(ref) <= 1e-13
+
+
+@pytest.mark.parametrize("S,H1", [(16, 129), (36, 129), (64, 1025), (81, 25), (125, 89)])
+def test_chol_solves_match_numpy(S, H1):
+    rng = np.random.default_rng(S)
+    Mk = rng.standard_normal((S, 4 * S))
+    G = Mk @ Mk.T
+    mu = 0.1 + rng.random(H1)
+    Fr = rng.standard_normal((H1, S))
+    Fi = rng.standard_normal((H1, S))
+    xr, xi, _ = _native.selftest_chol(G, mu, Fr, Fi)
+    for w in range(0, H1, max(1, H1 // 17)):
+        H = G + mu[w] * np.eye(S)
+        np.testing.assert_allclose(H @ xr[w], Fr[w], rtol=1e-9, atol=1e-9 * np.abs(Fr[w]).max())
+        np.testing.assert_allclose(H @ xi[w], Fi[w], rtol=1e-9, atol=1e-9 * np.abs(Fi[w]).max())

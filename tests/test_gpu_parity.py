@@ -68,8 +68,9 @@ def test_gpu_matches_oracle_fp64_configs(name, iters):
 
 @pytest.mark.parametrize("name,dims,iters", [("c4", (256, 256, 64), 20), ("c5", (20, 20, 20, 20, 20), 20)])
 def test_gpu_fp32_variant_scaled(name, dims, iters):
-    """FP32 variant against the FP64 oracle on the same (fp32-rounded) data:
-    bound 5e-3 relative in X, |dPSNR| <= 0.01 dB (north_star)."""
+    """FP32 variant (3xTF32 tensor-core products, FP64 solves) against the FP64
+    oracle on the same (fp32-rounded) data: bound 2e-4 relative in X (measured
+    2.6e-5 / 3.9e-5 at these shapes), |dPSNR| <= 0.01 dB (north_star)."""
     wl, truth, mask = make_instance(name, dims=dims)
     kw = dict(lam=0.35, delta=0.5, rho=0.1, eps=0.0, max_iters=iters, max_rank=wl.rank, initial_rank=wl.rank,
               rank_policy="fixed", algorithm="afctnlr", shuffle=True, seed=0)
@@ -77,7 +78,7 @@ def test_gpu_fp32_variant_scaled(name, dims, iters):
     res = P.run(P.Observation(truth, mask), P.SolverConfig(**kw), dtype="float32")
     peak = float(np.max(np.abs(truth)))
     dpsnr = abs(O.psnr(res.x, truth, peak) - O.psnr(ref.x, truth, peak))
-    assert rel(res.x, ref.x) <= 5e-3
+    assert rel(res.x, ref.x) <= 2e-4
     assert dpsnr <= 0.01
     m = mask
     assert np.array_equal(res.x[m], truth.astype(np.float32).astype(np.float64)[m])
