@@ -175,7 +175,10 @@ int fctn_timer(fctn_ctx* ctx, int op, double* ms);
 #define FCTN_K_COMPOSE 5  /* K4 compose + blend + reductions */
 #define FCTN_K_DFT 6      /* K3 forward / inverse DFT along mode k (+ factor write, stats) */
 #define FCTN_K_FGRAM 7    /* K3 factor Gram E_k = A_(k)^T A_(k) + stats fold */
-#define FCTN_K_COUNT 8
+#define FCTN_K_ZPASS 8    /* N=3 schedule: Z_0 = X x_0 A_(0) (tensor-core pass over X) */
+#define FCTN_K_YSMALL 9   /* N=3 schedule: Y_k = Z_0 (*) A_(l) (small contraction) */
+#define FCTN_K_MBUILD 10  /* M_k built outside the reference chain (compose operand) */
+#define FCTN_K_COUNT 12
 int fctn_set_profiling(fctn_ctx* ctx, int on);
 int fctn_get_profile(fctn_ctx* ctx, double* ms, int64_t* launches, double* bytes);
 

@@ -27,7 +27,8 @@ EXPORTS = [
     "fctn_sync", "fctn_selftest_stream", "fctn_selftest_chol", "fctn_timer", "fctn_set_profiling", "fctn_get_profile", "fctn_last_error", "fctn_version",
     "fctn_destroy",
 ]
-K_CLASSES = ["merge", "stream_y", "gram", "reduce", "chol", "compose", "dft", "fgram"]
+K_CLASSES = ["merge", "stream_y", "gram", "reduce", "chol", "compose", "dft", "fgram", "zpass", "ysmall", "mbuild",
+             "k11"]
 
 _lib = None
 
@@ -337,11 +338,11 @@ class Context:
         self._check(lib().fctn_set_profiling(self.h, int(bool(on))))
 
     def get_profile(self) -> dict:
-        ms = np.zeros(8)
-        n = np.zeros(8, dtype=np.int64)
-        b = np.zeros(8)
+        ms = np.zeros(12)
+        n = np.zeros(12, dtype=np.int64)
+        b = np.zeros(12)
         self._check(lib().fctn_get_profile(self.h, ms.ctypes.data_as(C.POINTER(C.c_double)),
                                            n.ctypes.data_as(C.POINTER(C.c_int64)),
                                            b.ctypes.data_as(C.POINTER(C.c_double))))
         return {K_CLASSES[i]: {"ms": float(ms[i]), "launches": int(n[i]), "bytes": float(b[i])}
-                for i in range(8) if n[i] > 0}
+                for i in range(12) if n[i] > 0}

@@ -152,6 +152,7 @@ class Ctx : public Executor {
     int64_t n;
   };
   bool prof = false;
+  int prof_cls = FCTN_K_MERGE;  // class of generic contractions (merge unless set)
   std::vector<Mark> marks;
   std::vector<cudaEvent_t> evpool;
   double prof_ms[FCTN_K_COUNT] = {0};
@@ -299,7 +300,7 @@ class Ctx : public Executor {
   void contract(const ContractOp& op) override {
     bool sw = false;
     ContractDesc d = desc_for(op, &sw);
-    int pm = pbegin(FCTN_K_MERGE);
+    int pm = pbegin(prof_cls);
     const void* ra = ptr_of(sw ? op.b : op.a);
     const void* cb = ptr_of(sw ? op.a : op.b);
     void* out = ptr_of(op.out);
@@ -747,7 +748,7 @@ class Ctx : public Executor {
   void compute_z0() {
     const int64_t T = sh.total();
     const int64_t I0 = sh.dims[0], p0 = T / I0, S0 = sh.s_of(0);
-    int pm = pbegin(FCTN_K_STREAM_Y);
+    int pm = pbegin(FCTN_K_ZPASS);
     if (dtype == FCTN_F32) {
       // the stream kernel with the roles of the modes swapped: rows = (i1, i2),
       // K = i0 (X's contiguous mode, K-major tiles), B = A_(0)
@@ -776,7 +777,7 @@ class Ctx : public Executor {
     op.out.labels = sh.factor_labels(k);
     bool sw = false;
     ContractDesc d = desc_for(op, &sw);
-    int pm = pbegin(FCTN_K_STREAM_Y);
+    int pm = pbegin(FCTN_K_YSMALL);
     if (dtype == FCTN_F32) {
       const float *pa = (const float*)Zbuf, *pb = (const float*)Ac[l];
       launch_contract<float>(sw ? pb : pa, sw ? pa : pb, (float*)ypart, d, (float*)cscratch, 2 * cscratch_cap, n_sm, st);
@@ -803,7 +804,10 @@ class Ctx : public Executor {
     op.b.factor = rest[1];
     op.out.labels = sh.m_labels(k);
     op.out.buf = M_ID;
+    const int cls = prof_cls;
+    prof_cls = FCTN_K_MBUILD;
     contract(op);
+    prof_cls = cls;
     mbuf_holds = k;
   }
 
