@@ -316,9 +316,10 @@ __global__ void __launch_bounds__(THREADS, 1)
 // each slot in place and one thread TMA-stores it back as X_new, keeping a
 // few bulk groups in flight.  The bulk engines, not registers, hold the bytes
 // in flight.  Operands stream through 16-row K stages.
-constexpr int KB2 = 16;      // K rows per operand stage
+constexpr int KB2 = 8;       // K rows per operand stage (one K=8 MMA step)
+constexpr int BOXB = 32 * KB2 * 4;  // bytes of one 32-row MN-major operand box
 constexpr int XC = 32;       // columns per X sub-tile
-constexpr int XS = 6;        // X ring slots
+constexpr int XS = 9;        // X ring slots
 constexpr int XKEEP = 3;     // TMA stores allowed in flight
 constexpr int T_CONV0 = 3, T_EPI0 = T_CONV0 + CONV_WARPS, T_NWARPS = T_EPI0 + EPI_WARPS;
 constexpr int T_THREADS = 32 * T_NWARPS;
@@ -417,17 +418,17 @@ __global__ void __launch_bounds__(T_THREADS, 1)
         tc::mbar_expect_tx(&full[s], tx);
         uint8_t* st = smem + s * STAGE;
 #pragma unroll
-        for (int c = 0; c < 4; ++c) tc::tma_load_2d(st + c * 2048, &tmA, &full[s], r0 + 32 * c, kb * KB2);
+        for (int c = 0; c < 4; ++c) tc::tma_load_2d(st + c * BOXB, &tmA, &full[s], r0 + 32 * c, kb * KB2);
 #pragma unroll
         for (int c = 0; c < N / 32; ++c)
-          tc::tma_load_2d(st + A_B + c * 2048, &tmB, &full[s], c0 + 32 * c, kb * KB2);
+          tc::tma_load_2d(st + A_B + c * BOXB, &tmB, &full[s], c0 + 32 * c, kb * KB2);
         if (SPLIT && args.a_pre)
 #pragma unroll
-          for (int c = 0; c < 4; ++c) tc::tma_load_2d(st + HI + c * 2048, &tmAl, &full[s], r0 + 32 * c, kb * KB2);
+          for (int c = 0; c < 4; ++c) tc::tma_load_2d(st + HI + c * BOXB, &tmAl, &full[s], r0 + 32 * c, kb * KB2);
         if (SPLIT && args.b_pre)
 #pragma unroll
           for (int c = 0; c < N / 32; ++c)
-            tc::tma_load_2d(st + HI + A_B + c * 2048, &tmBl, &full[s], c0 + 32 * c, kb * KB2);
+            tc::tma_load_2d(st + HI + A_B + c * BOXB, &tmBl, &full[s], c0 + 32 * c, kb * KB2);
       }
     }
   } else if (warp == 2 && lane == 0) {
@@ -460,12 +461,12 @@ __global__ void __launch_bounds__(T_THREADS, 1)
         const uint32_t a = tc::smem_u32(smem + s * STAGE), b = a + A_B;
 #pragma unroll
         for (int kk = 0; kk < KB2 / 8; ++kk) {
-          const uint64_t ad = tc::sdesc(a + kk * 1024, 2048, 512, 1);
-          const uint64_t bd = tc::sdesc(b + kk * 1024, 2048, 512, 1);
+          const uint64_t ad = tc::sdesc(a + kk * 1024, BOXB, 512, 1);
+          const uint64_t bd = tc::sdesc(b + kk * 1024, BOXB, 512, 1);
           const uint32_t first = (kb | kk) != 0;
           if (SPLIT) {
-            tc::mma_tf32(tmem + acc * N, tc::sdesc(a + HI + kk * 1024, 2048, 512, 1), bd, idesc, first);
-            tc::mma_tf32(tmem + acc * N, ad, tc::sdesc(b + HI + kk * 1024, 2048, 512, 1), idesc, 1);
+            tc::mma_tf32(tmem + acc * N, tc::sdesc(a + HI + kk * 1024, BOXB, 512, 1), bd, idesc, first);
+            tc::mma_tf32(tmem + acc * N, ad, tc::sdesc(b + HI + kk * 1024, BOXB, 512, 1), idesc, 1);
           }
           tc::mma_tf32(tmem + acc * N, ad, bd, idesc, SPLIT ? 1u : first);
         }

@@ -131,6 +131,7 @@ class Ctx : public Executor {
   void* Zbuf = nullptr;
   void* presplit = nullptr;     // fp32 [A hi | A lo | M hi | M lo] for the TC compose
   int64_t presplit_m_cap = 0;   // largest M_k (entries) that is pre-split
+  int64_t max_is_ = 0;          // largest factor unfolding (entries), presplit layout
   int64_t z_version = -1;
   int mbuf_holds = -1;   // mode whose M_k currently sits in Mbuf (-1: none)
   bool zroute = true;    // FCTN_NO_ZROUTE=1 disables
@@ -451,6 +452,7 @@ class Ctx : public Executor {
     }
     CK(cudaMalloc(&Ascratch, max_is * sizeof(double)));
     CK(cudaMalloc(&Mbuf, max_m * esize));
+    max_is_ = max_is;
     if (dtype == FCTN_F32) {
       presplit_m_cap = std::min<int64_t>(max_m, T / 4);
       CK(cudaMalloc(&presplit, (2 * max_is + 2 * presplit_m_cap) * sizeof(float)));
@@ -755,7 +757,16 @@ class Ctx : public Executor {
       TcStreamPlan tp = plan_stream_tc(p0, I0, 1, S0, n_sm, split3);
       tp.kb_per_split = tp.nkb;
       tp.nsplit = 1;
-      launch_stream_tc((const float*)X[cur], (const float*)fac_ptr(0), (float*)Zbuf, p0, I0, 1, S0, tp, st);
+      const float* bh = (const float*)fac_ptr(0);
+      const float* bl = nullptr;
+      if (split3) {  // A_(0) is tiny: split it once in HBM
+        float* h = (float*)presplit;
+        launch_tf32_split(bh, h, h + max_is_, I0 * S0, st);
+        bh = h;
+        bl = h + max_is_;
+        ++launches;
+      }
+      launch_stream_tc((const float*)X[cur], bh, (float*)Zbuf, p0, I0, 1, S0, tp, st, bl);
     } else {
       StreamPlan sp = plan_stream(p0, S0, I0, target_ctas());
       launch_stream<double>((const double*)X[cur], (const double*)fac_ptr(0), ypart, p0, I0, S0, I0, sp, st);
@@ -832,7 +843,16 @@ class Ctx : public Executor {
     const bool tc = tc_ok(k);
     if (tc) {
       TcStreamPlan tp = plan_stream_tc(I, P, p / P, S, n_sm, split3);
-      launch_stream_tc((const float*)X[cur], (const float*)Mbuf, (float*)ypart, I, P, p / P, S, tp, st);
+      const float* mh = (const float*)Mbuf;
+      const float* ml = nullptr;
+      if (split3 && S * p <= presplit_m_cap) {  // small M_k: split once in HBM, not per CTA in smem
+        float* h = (float*)presplit + 2 * max_is_ + 0;
+        launch_tf32_split((const float*)Mbuf, h, h + presplit_m_cap, S * p, st);
+        mh = h;
+        ml = h + presplit_m_cap;
+        ++launches;
+      }
+      launch_stream_tc((const float*)X[cur], mh, (float*)ypart, I, P, p / P, S, tp, st, ml);
       nsplit = (int)tp.nsplit;
     } else {
       StreamPlan sy = plan_stream(I, S, p, target_ctas());
@@ -908,13 +928,13 @@ class Ctx : public Executor {
       op.a = (const float*)fac_ptr(k);
       op.m = (const float*)Mbuf;
       float* ah = (float*)presplit;
-      float* al = split3 ? ah + I * S : nullptr;
+      float* al = split3 ? ah + max_is_ : nullptr;
       launch_tf32_split(op.a, ah, al, I * S, st);
       op.a_hi = ah;
       op.a_lo = al;
       if (S * p <= presplit_m_cap) {
-        float* mh = ah + 2 * I * S;
-        float* ml = split3 ? mh + S * p : nullptr;
+        float* mh = ah + 2 * max_is_;
+        float* ml = split3 ? mh + presplit_m_cap : nullptr;
         launch_tf32_split(op.m, mh, ml, S * p, st);
         op.m_hi = mh;
         op.m_lo = ml;

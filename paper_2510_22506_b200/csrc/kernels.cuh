@@ -77,8 +77,10 @@ struct TcStreamPlan {
 };
 bool tc_stream_supported(int64_t I, int64_t P, int64_t Q, int64_t S);
 TcStreamPlan plan_stream_tc(int64_t I, int64_t P, int64_t Q, int64_t S, int n_sm, bool split3);
+// Mlo: optional pre-split low part of M (then M holds rn_tf32 hi); with
+// split3 only the streamed X tile is split in shared memory
 void launch_stream_tc(const float* X, const float* M, float* part, int64_t I, int64_t P, int64_t Q, int64_t S,
-                      const TcStreamPlan& tp, cudaStream_t st);
+                      const TcStreamPlan& tp, cudaStream_t st, const float* Mlo = nullptr);
 
 // ---------------------------------------------------------------- K3 solve
 struct DftPlan {

@@ -49,7 +49,8 @@ struct StreamSmem {
 template <int NT, bool AMN, bool SPLIT>
 __global__ void __launch_bounds__(192, 1)
     k_stream_tc(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmM,
-                float* __restrict__ part, int I, int S, long long nkb_total, long long kb_per_split, int nPB) {
+                const __grid_constant__ CUtensorMap tmMl, float* __restrict__ part, int I, int S, long long nkb_total,
+                long long kb_per_split, int nPB, int b_pre) {
   using L = StreamSmem<NT, SPLIT>;
   constexpr int STAGES = L::STAGES;
   extern __shared__ uint8_t smem_raw[];
@@ -93,7 +94,7 @@ __global__ void __launch_bounds__(192, 1)
       const int s = it % STAGES;
       const uint32_t ph = (it / STAGES) & 1;
       tc::mbar_wait(&empty[s], ph ^ 1);
-      tc::mbar_expect_tx(&full[s], L::TMA_BYTES);
+      tc::mbar_expect_tx(&full[s], L::TMA_BYTES + ((SPLIT && b_pre) ? L::B_BYTES : 0));
       const long long kb = kb0 + it;
       uint8_t* a = smem + s * L::STAGE_BYTES;
       uint8_t* b = a + A_BYTES;
@@ -102,11 +103,13 @@ __global__ void __launch_bounds__(192, 1)
 #pragma unroll
         for (int c = 0; c < 4; ++c) tc::tma_load_2d(a + c * 4096, &tmX, &full[s], i0 + 32 * c, q0);
         tc::tma_load_2d(b, &tmM, &full[s], q0, 0);
+        if (SPLIT && b_pre) tc::tma_load_2d(b + L::TMA_BYTES, &tmMl, &full[s], q0, 0);
       } else {
         const int pb = (int)(kb % nPB) * BK;
         const int q = (int)(kb / nPB);
         tc::tma_load_3d(a, &tmX, &full[s], pb, i0, q);
         tc::tma_load_3d(b, &tmM, &full[s], pb, q, 0);
+        if (SPLIT && b_pre) tc::tma_load_3d(b + L::TMA_BYTES, &tmMl, &full[s], pb, q, 0);
       }
     }
   } else if (warp == 1 && lane == 0) {
@@ -142,7 +145,8 @@ __global__ void __launch_bounds__(192, 1)
       const int s = it % STAGES;
       tc::mbar_wait(&full[s], (it / STAGES) & 1);
       uint8_t* a = smem + s * L::STAGE_BYTES;
-      tc::tf32_split_tile<SPLIT>(a, a + L::TMA_BYTES, L::TMA_BYTES / 4, ct, 128);
+      // a pre-split B (hi/lo from HBM) leaves only the X tile to convert
+      tc::tf32_split_tile<SPLIT>(a, a + L::TMA_BYTES, (b_pre ? A_BYTES : L::TMA_BYTES) / 4, ct, 128);
       tc::fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(&conv[s]);
@@ -200,25 +204,26 @@ CUtensorMap make_map(const void* base, int rank, const uint64_t* dims, const uin
 }
 
 template <int NT, bool AMN, bool SPLIT>
-void go3(const CUtensorMap& mx, const CUtensorMap& mm, float* part, int64_t I, int64_t S, const TcStreamPlan& tp,
-         cudaStream_t st) {
+void go3(const CUtensorMap& mx, const CUtensorMap& mm, const CUtensorMap& mml, bool b_pre, float* part, int64_t I,
+         int64_t S, const TcStreamPlan& tp, cudaStream_t st) {
   const int smem = StreamSmem<NT, SPLIT>::TOTAL;
   auto fn = k_stream_tc<NT, AMN, SPLIT>;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) throw std::runtime_error(std::string("stream_tc smem: ") + cudaGetErrorString(e));
   dim3 grid((unsigned)tp.n_mtiles, (unsigned)tp.nsplit);
-  fn<<<grid, 192, smem, st>>>(mx, mm, part, (int)I, (int)S, tp.nkb, tp.kb_per_split, (int)tp.npb);
+  fn<<<grid, 192, smem, st>>>(mx, mm, mml, part, (int)I, (int)S, tp.nkb, tp.kb_per_split, (int)tp.npb,
+                              b_pre ? 1 : 0);
   e = cudaGetLastError();
   if (e != cudaSuccess) throw std::runtime_error(std::string("stream_tc: ") + cudaGetErrorString(e));
 }
 
 template <int NT, bool AMN>
-void go(const CUtensorMap& mx, const CUtensorMap& mm, float* part, int64_t I, int64_t S, const TcStreamPlan& tp,
-        cudaStream_t st) {
+void go(const CUtensorMap& mx, const CUtensorMap& mm, const CUtensorMap& mml, bool b_pre, float* part, int64_t I,
+        int64_t S, const TcStreamPlan& tp, cudaStream_t st) {
   if (tp.split3)
-    go3<NT, AMN, true>(mx, mm, part, I, S, tp, st);
+    go3<NT, AMN, true>(mx, mm, mml, b_pre, part, I, S, tp, st);
   else
-    go3<NT, AMN, false>(mx, mm, part, I, S, tp, st);
+    go3<NT, AMN, false>(mx, mm, mml, b_pre, part, I, S, tp, st);
 }
 
 }  // namespace
@@ -257,8 +262,9 @@ TcStreamPlan plan_stream_tc(int64_t I, int64_t P, int64_t Q, int64_t S, int n_sm
 }
 
 void launch_stream_tc(const float* X, const float* M, float* part, int64_t I, int64_t P, int64_t Q, int64_t S,
-                      const TcStreamPlan& tp, cudaStream_t st) {
-  CUtensorMap mx, mm;
+                      const TcStreamPlan& tp, cudaStream_t st, const float* Mlo) {
+  CUtensorMap mx, mm, mml;
+  const bool b_pre = Mlo != nullptr && tp.split3;
   if (P == 1) {
     uint64_t dx[2] = {(uint64_t)I, (uint64_t)Q}, sx[1] = {(uint64_t)I * 4};
     uint32_t bx[2] = {32, 32};
@@ -266,6 +272,7 @@ void launch_stream_tc(const float* X, const float* M, float* part, int64_t I, in
     uint64_t dm[2] = {(uint64_t)Q, (uint64_t)S}, sm[1] = {(uint64_t)Q * 4};
     uint32_t bm[2] = {32, (uint32_t)tp.nt};
     mm = make_map(M, 2, dm, sm, bm);
+    mml = b_pre ? make_map(Mlo, 2, dm, sm, bm) : mm;
   } else {
     uint64_t dx[3] = {(uint64_t)P, (uint64_t)I, (uint64_t)Q}, sx[2] = {(uint64_t)P * 4, (uint64_t)P * I * 4};
     uint32_t bx[3] = {32, 128, 1};
@@ -273,13 +280,14 @@ void launch_stream_tc(const float* X, const float* M, float* part, int64_t I, in
     uint64_t dm[3] = {(uint64_t)P, (uint64_t)Q, (uint64_t)S}, sm[2] = {(uint64_t)P * 4, (uint64_t)P * Q * 4};
     uint32_t bm[3] = {32, 1, (uint32_t)tp.nt};
     mm = make_map(M, 3, dm, sm, bm);
+    mml = b_pre ? make_map(Mlo, 3, dm, sm, bm) : mm;
   }
   const bool amn = P == 1;
   switch (tp.nt) {
-    case 32: amn ? go<32, true>(mx, mm, part, I, S, tp, st) : go<32, false>(mx, mm, part, I, S, tp, st); break;
-    case 64: amn ? go<64, true>(mx, mm, part, I, S, tp, st) : go<64, false>(mx, mm, part, I, S, tp, st); break;
-    case 96: amn ? go<96, true>(mx, mm, part, I, S, tp, st) : go<96, false>(mx, mm, part, I, S, tp, st); break;
-    default: amn ? go<128, true>(mx, mm, part, I, S, tp, st) : go<128, false>(mx, mm, part, I, S, tp, st); break;
+    case 32: amn ? go<32, true>(mx, mm, mml, b_pre, part, I, S, tp, st) : go<32, false>(mx, mm, mml, b_pre, part, I, S, tp, st); break;
+    case 64: amn ? go<64, true>(mx, mm, mml, b_pre, part, I, S, tp, st) : go<64, false>(mx, mm, mml, b_pre, part, I, S, tp, st); break;
+    case 96: amn ? go<96, true>(mx, mm, mml, b_pre, part, I, S, tp, st) : go<96, false>(mx, mm, mml, b_pre, part, I, S, tp, st); break;
+    default: amn ? go<128, true>(mx, mm, mml, b_pre, part, I, S, tp, st) : go<128, false>(mx, mm, mml, b_pre, part, I, S, tp, st); break;
   }
 }
 
