@@ -778,29 +778,20 @@ class Ctx : public Executor {
     z_version = planner->versions[0];
   }
   void y_from_z(int k) {
-    int l = 0;
-    for (int j = 1; j < 3; ++j)
-      if (j != k) l = j;
+    const int l = (k == 1) ? 2 : 1;
     const int64_t I = sh.dims[k], S = sh.s_of(k);
-    ContractOp op;
-    op.a.labels = z_labels();
-    op.b.labels = sh.factor_labels(l);
-    op.out.labels = sh.factor_labels(k);
-    bool sw = false;
-    ContractDesc d = desc_for(op, &sw);
+    const int R01 = (int)sh.tri[sh.tri_index(0, 1)], R02 = (int)sh.tri[sh.tri_index(0, 2)];
+    const int R12 = (int)sh.tri[sh.tri_index(1, 2)];
     int pm = pbegin(FCTN_K_YSMALL);
-    if (dtype == FCTN_F32) {
-      const float *pa = (const float*)Zbuf, *pb = (const float*)Ac[l];
-      launch_contract<float>(sw ? pb : pa, sw ? pa : pb, (float*)ypart, d, (float*)cscratch, 2 * cscratch_cap, n_sm, st);
-      launch_reduce_splits_f32((const float*)ypart, 1, I * S, sharded() ? nullptr : A64[k], rho, Y, st);
-    } else {
-      const double *pa = (const double*)Zbuf, *pb = A64[l];
-      launch_contract<double>(sw ? pb : pa, sw ? pa : pb, ypart, d, cscratch, cscratch_cap, n_sm, st);
-      launch_reduce_splits(ypart, 1, I * S, sharded() ? nullptr : A64[k], rho, Y, st);
-    }
-    launches += 3;
+    if (dtype == FCTN_F32)
+      launch_y_from_z<float>((const float*)Zbuf, (const float*)Ac[l], k, sh.dims[1], sh.dims[2], R01, R02, R12, Y,
+                             st);
+    else
+      launch_y_from_z<double>((const double*)Zbuf, A64[l], k, sh.dims[1], sh.dims[2], R01, R02, R12, Y, st);
+    if (!sharded()) launch_axpy(Y, A64[k], rho, I * S, st);  // + rho A_prev (sylvester.py:106)
+    launches += 2;
+    pend(pm, (double)esize * ((sh.total() / sh.dims[0]) * sh.s_of(0)) + 8.0 * I * S, 2);
     if (sharded()) finish_y(k, false);  // Z_0 summed over this slab only
-    pend(pm, (double)esize * (d.rows * d.cols + (sh.total() / sh.dims[0]) * sh.s_of(0)), 3);
   }
   // M_j of the current factors into Mbuf, outside the reference's chain (no meter)
   void build_m_direct(int k) {
