@@ -132,6 +132,7 @@ class Ctx : public Executor {
   void* presplit = nullptr;     // fp32 [A hi | A lo | M hi | M lo] for the TC compose
   int64_t presplit_m_cap = 0;   // largest M_k (entries) that is pre-split
   int64_t max_is_ = 0;          // largest factor unfolding (entries), presplit layout
+  int64_t ypart_cap = 0;        // doubles in ypart
   int64_t z_version = -1;
   int mbuf_holds = -1;   // mode whose M_k currently sits in Mbuf (-1: none)
   bool zroute = true;    // FCTN_NO_ZROUTE=1 disables
@@ -428,6 +429,9 @@ class Ctx : public Executor {
       max_part = std::max(max_part, ((I + 63) / 64) * ((p + 63) / 64));
       max_ep = std::max(max_ep, (int64_t)fgram_splits(Ig) * S * S);
     }
+    if (n == 3)  // Y_1 partials of the Z route (split over b02)
+      max_yp = std::max(max_yp, sh.tri[sh.tri_index(0, 2)] * sh.dims[1] * sh.tri[sh.tri_index(0, 1)] *
+                                    sh.tri[sh.tri_index(1, 2)]);
     A64.assign(n, nullptr);
     Ac.assign(n, nullptr);
     E64.assign(n, nullptr);
@@ -465,6 +469,7 @@ class Ctx : public Executor {
     CK(cudaMalloc(&Fr, max_h * sizeof(double)));
     CK(cudaMalloc(&Fi, max_h * sizeof(double)));
     CK(cudaMalloc(&ypart, max_yp * sizeof(double)));
+    ypart_cap = max_yp;
     CK(cudaMalloc(&epart, max_ep * sizeof(double)));
     CK(cudaMalloc(&colstats, max_s * 3 * sizeof(double)));
     partial_cap = std::max<int64_t>(max_part, 4 * n_sm);
@@ -733,6 +738,13 @@ class Ctx : public Executor {
   // come from the planner's replay of the reference chain.
   bool z_route(int k) const {
     if (sh.n != 3 || k == 0 || !zroute || !Zbuf) return false;
+    {
+      const int64_t R01 = sh.tri[sh.tri_index(0, 1)], R02 = sh.tri[sh.tri_index(0, 2)];
+      const int64_t R12 = sh.tri[sh.tri_index(1, 2)];
+      if (k == 2 && !(R01 == R12 && R01 <= 8)) return false;
+      if (R12 > 16) return false;
+      if (k == 1 && R02 * sh.dims[1] * R01 * R12 > ypart_cap) return false;
+    }
     if (dtype == FCTN_F32 && !(use_tc && tc_stream_supported(sh.total() / sh.dims[0], sh.dims[0], 1, sh.s_of(0))))
       return false;
     if (z_version == planner->versions[0]) return true;  // fresh: no pass over X at all
@@ -785,9 +797,9 @@ class Ctx : public Executor {
     int pm = pbegin(FCTN_K_YSMALL);
     if (dtype == FCTN_F32)
       launch_y_from_z<float>((const float*)Zbuf, (const float*)Ac[l], k, sh.dims[1], sh.dims[2], R01, R02, R12, Y,
-                             st);
+                             ypart, st);
     else
-      launch_y_from_z<double>((const double*)Zbuf, A64[l], k, sh.dims[1], sh.dims[2], R01, R02, R12, Y, st);
+      launch_y_from_z<double>((const double*)Zbuf, A64[l], k, sh.dims[1], sh.dims[2], R01, R02, R12, Y, ypart, st);
     if (!sharded()) launch_axpy(Y, A64[k], rho, I * S, st);  // + rho A_prev (sylvester.py:106)
     launches += 2;
     pend(pm, (double)esize * ((sh.total() / sh.dims[0]) * sh.s_of(0)) + 8.0 * I * S, 2);

@@ -457,80 +457,119 @@ void launch_axpy(double* y, const double* x, double a, int64_t n, cudaStream_t s
 
 // N = 3 schedule, Y_k = Z_0 (*) A_(l) with Z_0 = [i1, i2, b01, b02] (i1 fastest):
 //  k = 2: Y[i2, b02, b12] = sum_{i1, b01} Z[i1, i2, b01, b02] A1[i1, b01, b12]
-//         one CTA per (i2, b02); threads stride i1 (coalesced), fixed-order tree
+//         CTA per (b02, group of G i2); a thread keeps A1[i1, :, :] in registers
+//         for its i1 and accumulates G x R12 sums; fixed-order block tree.
 //  k = 1: Y[i1, b01, b12] = sum_{i2, b02} Z[i1, i2, b01, b02] A2[i2, b02, b12]
-//         one thread per (i1, b01); A2 values are warp-uniform
+//         thread per (i1, b01), CTAs also split b02 (partials reduced in order);
+//         A2 values are warp-uniform.
 // fp64 accumulation, deterministic.
-template <typename T, int RB>
+template <typename T, int R01, int R12, int G>
 __global__ void __launch_bounds__(256) k_yz2(const T* __restrict__ Z, const T* __restrict__ A1, int64_t I1,
-                                             int64_t I2, int R01, int R02, int R12, double* __restrict__ Y) {
-  const int64_t i2 = blockIdx.x % I2, b02 = blockIdx.x / I2;
-  double acc[RB];
+                                             int64_t I2, int R02, double* __restrict__ Y) {
+  const int64_t b02 = blockIdx.x % R02, i2_0 = (blockIdx.x / R02) * G;
+  double acc[G][R12];
 #pragma unroll
-  for (int c = 0; c < RB; ++c) acc[c] = 0.0;
-  for (int64_t i1 = threadIdx.x; i1 < I1; i1 += 256)
-    for (int b01 = 0; b01 < R01; ++b01) {
-      const double z = (double)Z[i1 + I1 * (i2 + I2 * (b01 + (int64_t)R01 * b02))];
+  for (int g = 0; g < G; ++g)
 #pragma unroll
-      for (int c = 0; c < RB; ++c)
-        if (c < R12) acc[c] += z * (double)A1[i1 + I1 * (b01 + (int64_t)R01 * c)];
+    for (int c = 0; c < R12; ++c) acc[g][c] = 0.0;
+  for (int64_t i1 = threadIdx.x; i1 < I1; i1 += 256) {
+    float a[R01][R12];
+#pragma unroll
+    for (int b = 0; b < R01; ++b)
+#pragma unroll
+      for (int c = 0; c < R12; ++c) a[b][c] = (float)A1[i1 + I1 * (b + (int64_t)R01 * c)];
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      const int64_t i2 = i2_0 + g;
+      if (i2 >= I2) break;
+#pragma unroll
+      for (int b = 0; b < R01; ++b) {
+        const double z = (double)Z[i1 + I1 * (i2 + I2 * (b + (int64_t)R01 * b02))];
+#pragma unroll
+        for (int c = 0; c < R12; ++c) acc[g][c] += z * (double)a[b][c];
+      }
     }
-  __shared__ double red[8][RB];
+  }
+  __shared__ double red[8][G * R12];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
 #pragma unroll
-  for (int c = 0; c < RB; ++c) {
-    double v = acc[c];
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    if (lane == 0) red[wid][c] = v;
-  }
+  for (int g = 0; g < G; ++g)
+#pragma unroll
+    for (int c = 0; c < R12; ++c) {
+      double v = acc[g][c];
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (lane == 0) red[wid][g * R12 + c] = v;
+    }
   __syncthreads();
-  if (threadIdx.x < R12) {
+  for (int e = threadIdx.x; e < G * R12; e += 256) {
+    const int g = e / R12, c = e % R12;
+    const int64_t i2 = i2_0 + g;
+    if (i2 >= I2) continue;
     double v = 0.0;
-    for (int q = 0; q < 8; ++q) v += red[q][threadIdx.x];
-    Y[i2 + I2 * (b02 + (int64_t)R02 * threadIdx.x)] = v;
+    for (int q = 0; q < 8; ++q) v += red[q][e];
+    Y[i2 + I2 * (b02 + (int64_t)R02 * c)] = v;
   }
 }
 
 template <typename T, int RB>
 __global__ void __launch_bounds__(256) k_yz1(const T* __restrict__ Z, const T* __restrict__ A2, int64_t I1,
-                                             int64_t I2, int R01, int R02, int R12, double* __restrict__ Y) {
+                                             int64_t I2, int R01, int R02, int R12, double* __restrict__ part) {
   const int64_t i1 = blockIdx.x * 256LL + threadIdx.x;
-  const int b01 = blockIdx.y;
+  const int b01 = blockIdx.y, b02 = blockIdx.z;
   if (i1 >= I1) return;
   double acc[RB];
 #pragma unroll
   for (int c = 0; c < RB; ++c) acc[c] = 0.0;
-  for (int b02 = 0; b02 < R02; ++b02)
-    for (int64_t i2 = 0; i2 < I2; ++i2) {
-      const double z = (double)Z[i1 + I1 * (i2 + I2 * (b01 + (int64_t)R01 * b02))];
+  for (int64_t i2 = 0; i2 < I2; ++i2) {
+    const double z = (double)Z[i1 + I1 * (i2 + I2 * (b01 + (int64_t)R01 * b02))];
 #pragma unroll
-      for (int c = 0; c < RB; ++c)
-        if (c < R12) acc[c] += z * (double)__ldg(A2 + i2 + I2 * (b02 + (int64_t)R02 * c));
-    }
+    for (int c = 0; c < RB; ++c)
+      if (c < R12) acc[c] += z * (double)__ldg(A2 + i2 + I2 * (b02 + (int64_t)R02 * c));
+  }
+  const int64_t n = I1 * R01 * R12;
 #pragma unroll
   for (int c = 0; c < RB; ++c)
-    if (c < R12) Y[i1 + I1 * (b01 + (int64_t)R01 * c)] = acc[c];
+    if (c < R12) part[b02 * n + i1 + I1 * (b01 + (int64_t)R01 * c)] = acc[c];
+}
+
+template <typename T, int R01, int R12>
+static void yz2_go(const T* Z, const T* Al, int64_t I1, int64_t I2, int R02, double* Y, cudaStream_t st) {
+  constexpr int G = 8;
+  const unsigned grid = (unsigned)(R02 * ((I2 + G - 1) / G));
+  k_yz2<T, R01, R12, G><<<grid, 256, 0, st>>>(Z, Al, I1, I2, R02, Y);
 }
 
 template <typename T>
 void launch_y_from_z(const T* Z, const T* Al, int k, int64_t I1, int64_t I2, int R01, int R02, int R12, double* Y,
-                     cudaStream_t st) {
+                     double* part, cudaStream_t st) {
   if (R12 > 16) throw std::runtime_error("y_from_z: bond > 16");
   if (k == 2) {
-    const unsigned grid = (unsigned)(I2 * R02);
-    if (R12 <= 8) k_yz2<T, 8><<<grid, 256, 0, st>>>(Z, Al, I1, I2, R01, R02, R12, Y);
-    else k_yz2<T, 16><<<grid, 256, 0, st>>>(Z, Al, I1, I2, R01, R02, R12, Y);
-  } else {
-    dim3 grid((unsigned)((I1 + 255) / 256), (unsigned)R01);
-    if (R12 <= 8) k_yz1<T, 8><<<grid, 256, 0, st>>>(Z, Al, I1, I2, R01, R02, R12, Y);
-    else k_yz1<T, 16><<<grid, 256, 0, st>>>(Z, Al, I1, I2, R01, R02, R12, Y);
+    if (R01 == R12 && R01 <= 8) {
+      switch (R01) {
+        case 1: yz2_go<T, 1, 1>(Z, Al, I1, I2, R02, Y, st); break;
+        case 2: yz2_go<T, 2, 2>(Z, Al, I1, I2, R02, Y, st); break;
+        case 3: yz2_go<T, 3, 3>(Z, Al, I1, I2, R02, Y, st); break;
+        case 4: yz2_go<T, 4, 4>(Z, Al, I1, I2, R02, Y, st); break;
+        case 5: yz2_go<T, 5, 5>(Z, Al, I1, I2, R02, Y, st); break;
+        case 6: yz2_go<T, 6, 6>(Z, Al, I1, I2, R02, Y, st); break;
+        case 7: yz2_go<T, 7, 7>(Z, Al, I1, I2, R02, Y, st); break;
+        default: yz2_go<T, 8, 8>(Z, Al, I1, I2, R02, Y, st); break;
+      }
+      check_launch("y_from_z2");
+      return;
+    }
+    throw std::runtime_error("y_from_z: non-uniform bonds need the generic contraction");
   }
-  check_launch("y_from_z");
+  dim3 grid((unsigned)((I1 + 255) / 256), (unsigned)R01, (unsigned)R02);
+  if (R12 <= 8) k_yz1<T, 8><<<grid, 256, 0, st>>>(Z, Al, I1, I2, R01, R02, R12, part);
+  else k_yz1<T, 16><<<grid, 256, 0, st>>>(Z, Al, I1, I2, R01, R02, R12, part);
+  check_launch("y_from_z1");
+  launch_reduce_splits(part, R02, I1 * R01 * R12, nullptr, 0.0, Y, st);
 }
 template void launch_y_from_z<float>(const float*, const float*, int, int64_t, int64_t, int, int, int, double*,
-                                     cudaStream_t);
+                                     double*, cudaStream_t);
 template void launch_y_from_z<double>(const double*, const double*, int, int64_t, int64_t, int, int, int, double*,
-                                      cudaStream_t);
+                                      double*, cudaStream_t);
 
 __global__ void k_convert(const double* __restrict__ in, float* __restrict__ out, int64_t n) {
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)

@@ -39,7 +39,7 @@ void launch_convert_f32_f64(const float* in, double* out, int64_t n, cudaStream_
 // N = 3 schedule: Y_k (k = 1, 2) = Z_0 (*) A_(l), Z_0 = [i1, i2, b01, b02]; Y fp64 (I_k x s_k)
 template <typename T>
 void launch_y_from_z(const T* Z, const T* Al, int k, int64_t I1, int64_t I2, int R01, int R02, int R12, double* Y,
-                     cudaStream_t st);
+                     double* part, cudaStream_t st);
 // mode-0 sharding helpers (fctn_set_comm)
 void launch_copy_rows(const double* A, int64_t I, int64_t S, int64_t lo, int64_t rows, void* out, bool f32,
                       cudaStream_t st);
