@@ -473,11 +473,11 @@ __global__ void __launch_bounds__(256) k_yz2(const T* __restrict__ Z, const T* _
 #pragma unroll
     for (int c = 0; c < R12; ++c) acc[g][c] = 0.0;
   for (int64_t i1 = threadIdx.x; i1 < I1; i1 += 256) {
-    float a[R01][R12];
+    T a[R01][R12];
 #pragma unroll
     for (int b = 0; b < R01; ++b)
 #pragma unroll
-      for (int c = 0; c < R12; ++c) a[b][c] = (float)A1[i1 + I1 * (b + (int64_t)R01 * c)];
+      for (int c = 0; c < R12; ++c) a[b][c] = A1[i1 + I1 * (b + (int64_t)R01 * c)];
 #pragma unroll
     for (int g = 0; g < G; ++g) {
       const int64_t i2 = i2_0 + g;
