@@ -136,6 +136,11 @@ class Ctx : public Executor {
   int64_t z_version = -1;
   int mbuf_holds = -1;   // mode whose M_k currently sits in Mbuf (-1: none)
   bool zroute = true;    // FCTN_NO_ZROUTE=1 disables
+  // Three-mode sweeps have no data-dependent host decisions and no allocations,
+  // so each (visiting order, X buffer parity, extrapolation) sweep is captured
+  // once as a CUDA graph and replayed (FCTN_NO_GRAPH=1 disables).
+  bool use_graph = true;
+  std::map<std::string, std::pair<cudaGraphExec_t, int64_t>> graphs;  // -> (exec, launches)
   // mode-0 sharding: rows [slab_lo, slab_hi) of mode 0 live here
   int rank = 0, nranks = 1;
   int64_t slab_lo = 0, slab_hi = 0, slab_max = 0;
@@ -333,7 +338,12 @@ class Ctx : public Executor {
   }
 
   // ------------------------------------------------------------ setup
+  void drop_graphs() {
+    for (auto& kv : graphs) cudaGraphExecDestroy(kv.second.first);
+    graphs.clear();
+  }
   void release_shape_buffers() {
+    drop_graphs();
     for (auto& kv : bufs) cudaFree(kv.second);
     bufs.clear();
     cudaFree(cscratch);
@@ -665,6 +675,8 @@ class Ctx : public Executor {
     {
       const char* e = getenv("FCTN_NO_TC");
       use_tc = !(e && e[0] == '1');
+      const char* ng = getenv("FCTN_NO_GRAPH");
+      use_graph = !(ng && ng[0] == '1');
       const char* zr = getenv("FCTN_NO_ZROUTE");
       zroute = !(zr && zr[0] == '1');
       const char* t = getenv("FCTN_TF32");
@@ -910,8 +922,8 @@ class Ctx : public Executor {
     launch_factor_gram(Ascratch, I, S, epart, E64[k], colstats, dstats + 3 * k, st);
     pend(pm, 8.0 * (I * S + S * S), 2);
     if (mbuf_holds >= 0 && mbuf_holds != k) mbuf_holds = -1;  // M_j (j != k) contains A_k
-    std::swap(A64[k], Ascratch);
-    if (dtype == FCTN_F64) Ac[k] = A64[k];
+    // keep every factor at a fixed address (the sweep may be replayed as a CUDA graph)
+    CK(cudaMemcpyAsync(A64[k], Ascratch, I * S * sizeof(double), cudaMemcpyDeviceToDevice, st));
     launches += 7;
     planner->versions[k] += 1;  // network.py:200
     if (k == 0) refresh_slab();
@@ -978,20 +990,9 @@ class Ctx : public Executor {
     }
   }
 
-  void sweep(const int32_t* order_in, int extrap, double alpha, double beta, double* stats, int64_t* counters) {
-    if (!uploaded) throw UsageError("no data uploaded");
+  // all device work of one sweep (plus its host bookkeeping)
+  void sweep_device(const std::vector<int>& order, int extrap, double alpha, double beta) {
     const int n = sh.n;
-    std::vector<int> order(order_in, order_in + n);
-    {
-      std::vector<int> chk = order;
-      std::sort(chk.begin(), chk.end());
-      for (int i = 0; i < n; ++i)
-        if (chk[i] != i) throw UsageError("order is not a permutation of range(n)");
-    }
-    Meter m0 = planner->meter;
-    int64_t hits0 = planner->cache().hits;
-    launches = 0;
-    CK(cudaEventRecord(ev0, st));
     for (int k : order) {
       const bool zr = z_route(k);
       if (alg == FCTN_ALG_ACCEL) {
@@ -1022,6 +1023,121 @@ class Ctx : public Executor {
       planner->meter = keep;
       planner->meter.compose += planner->compose_chain_flops();
       compose(n - 1, false);
+    }
+  }
+
+  static std::string graph_key(const std::vector<int>& order, int cur_, int extrap, double alpha, double beta) {
+    std::string key;
+    for (int k : order) key += std::to_string(k) + ",";
+    return key + "|" + std::to_string(cur_) + "|" + std::to_string(extrap) + "|" + std::to_string(alpha) + "|" +
+           std::to_string(beta);
+  }
+  // capture all 3! orders x both X parities up front (nothing executes; the
+  // host bookkeeping of the captures is rolled back)
+  void precapture(int extrap, double alpha, double beta) {
+    const Meter meter0 = planner->meter;
+    const std::vector<int64_t> versions0 = planner->versions;
+    const int cur0 = cur, zv0 = z_version, mh0 = mbuf_holds;
+    const int64_t l0 = launches;
+    std::vector<int> order{0, 1, 2};
+    for (int parity = 0; parity < 2; ++parity) {
+      do {
+        cur = parity;
+        z_version = -1;
+        mbuf_holds = -1;
+        launches = 0;
+        const std::string key = graph_key(order, parity, extrap, alpha, beta);
+        if (graphs.count(key)) continue;
+        CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+        try {
+          sweep_device(order, extrap, alpha, beta);
+        } catch (...) {
+          cudaGraph_t g = nullptr;
+          cudaStreamEndCapture(st, &g);
+          if (g) cudaGraphDestroy(g);
+          throw;
+        }
+        cudaGraph_t g;
+        CK(cudaStreamEndCapture(st, &g));
+        cudaGraphExec_t ge;
+        CK(cudaGraphInstantiate(&ge, g, 0));
+        CK(cudaGraphDestroy(g));
+        graphs[key] = {ge, launches};
+      } while (std::next_permutation(order.begin(), order.end()));
+    }
+    planner->meter = meter0;
+    planner->versions = versions0;
+    cur = cur0;
+    z_version = zv0;
+    mbuf_holds = mh0;
+    launches = l0;
+  }
+
+  // the host-side effects of sweep_device without any device work (graph replay)
+  void sweep_bookkeeping(const std::vector<int>& order) {
+    const int64_t T = gsh.total();
+    for (int k : order) {
+      if (alg == FCTN_ALG_ACCEL)
+        planner->partial_cached(k, order, nullptr, M_ID);
+      else
+        planner->partial_plain(k, nullptr, M_ID);
+      const int64_t I = gsh.dims[k], S = gsh.s_of(k), p = T / I;
+      planner->meter.proj += 2 * I * p * S;  // sylvester.py:105
+      planner->meter.gram += 2 * S * S * p;  // sylvester.py:58
+      planner->versions[k] += 1;             // network.py:200
+    }
+    const int k_last = order.back();
+    if (alg == FCTN_ALG_ACCEL)
+      planner->meter.compose += 2 * (T / gsh.dims[k_last]) * gsh.s_of(k_last) * gsh.dims[k_last];
+    else
+      planner->meter.compose += planner->compose_chain_flops();
+  }
+
+  void sweep(const int32_t* order_in, int extrap, double alpha, double beta, double* stats, int64_t* counters) {
+    if (!uploaded) throw UsageError("no data uploaded");
+    const int n = sh.n;
+    std::vector<int> order(order_in, order_in + n);
+    {
+      std::vector<int> chk = order;
+      std::sort(chk.begin(), chk.end());
+      for (int i = 0; i < n; ++i)
+        if (chk[i] != i) throw UsageError("order is not a permutation of range(n)");
+    }
+    Meter m0 = planner->meter;
+    int64_t hits0 = planner->cache().hits;
+    launches = 0;
+    const bool graphable = use_graph && sh.n == 3 && !prof && comm.kind == 0 && !sharded();
+    const std::string key = graphable ? graph_key(order, cur, extrap, alpha, beta) : std::string();
+    if (graphable && graphs.empty()) precapture(extrap, alpha, beta);
+    auto it = graphable ? graphs.find(key) : graphs.end();
+    if (graphable && it != graphs.end()) {
+      // replay: host bookkeeping only (the reference's FLOP meter, cache,
+      // versions), then the captured device work
+      sweep_bookkeeping(order);
+      CK(cudaEventRecord(ev0, st));
+      CK(cudaGraphLaunch(it->second.first, st));
+      launches = it->second.second;
+    } else if (graphable) {
+      CK(cudaEventRecord(ev0, st));
+      CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+      try {
+        sweep_device(order, extrap, alpha, beta);
+      } catch (...) {
+        cudaGraph_t g;
+        cudaStreamEndCapture(st, &g);
+        if (g) cudaGraphDestroy(g);
+        throw;
+      }
+      cudaGraph_t g;
+      CK(cudaStreamEndCapture(st, &g));
+      cudaGraphExec_t ge;
+      CK(cudaGraphInstantiate(&ge, g, 0));
+      CK(cudaGraphDestroy(g));
+      graphs[key] = {ge, launches};
+      CK(cudaGraphLaunch(ge, st));
+    } else {
+      CK(cudaEventRecord(ev0, st));
+      sweep_device(order, extrap, alpha, beta);
     }
     CK(cudaEventRecord(ev1, st));
     fetch_stats();
