@@ -35,6 +35,8 @@ CUtensorMap tc_make_map_f32(const void* base, int rank, const uint64_t* dims, co
                             const uint32_t* box, bool mn32);
 CUtensorMap tc_make_map_f32_plain(const void* base, int rank, const uint64_t* dims, const uint64_t* strides_bytes,
                                   const uint32_t* box);
+CUtensorMap tc_make_map_u32_plain(const void* base, int rank, const uint64_t* dims, const uint64_t* strides_bytes,
+                                  const uint32_t* box);
 
 namespace {
 
@@ -324,6 +326,7 @@ constexpr int XKEEP = 3;     // TMA stores allowed in flight
 constexpr int T_CONV0 = 3, T_EPI0 = T_CONV0 + CONV_WARPS, T_NWARPS = T_EPI0 + EPI_WARPS;
 constexpr int T_THREADS = 32 * T_NWARPS;
 constexpr int XBYTES = 128 * XC * 4;
+constexpr int MBYTES = XC * 4 * 4;  // mask bits of a sub-tile: 4 words (128 rows) per column
 
 struct ComposeTmaArgs {
   const uint32_t* maskbits;
@@ -356,7 +359,7 @@ __global__ void __launch_bounds__(T_THREADS, 1)
     k_compose_tma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmAl,
                   const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUtensorMap tmBl,
                   const __grid_constant__ CUtensorMap tmXo, const __grid_constant__ CUtensorMap tmXn,
-                  const ComposeTmaArgs args) {
+                  const __grid_constant__ CUtensorMap tmMask, const ComposeTmaArgs args) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   constexpr uint32_t A_B = 128u * KB2 * 4u, B_B = (uint32_t)N * KB2 * 4u;
@@ -364,7 +367,8 @@ __global__ void __launch_bounds__(T_THREADS, 1)
   constexpr uint32_t STAGE = HI * (SPLIT ? 2 : 1);
   constexpr int OPS = 2;
   uint8_t* xring = smem + OPS * STAGE;
-  uint64_t* full = reinterpret_cast<uint64_t*>(xring + XS * XBYTES);
+  uint32_t* mring = reinterpret_cast<uint32_t*>(xring + XS * XBYTES);  // [XS][XC][4] mask words
+  uint64_t* full = reinterpret_cast<uint64_t*>(xring + XS * (XBYTES + MBYTES));
   uint64_t* conv = full + OPS;
   uint64_t* empty = conv + OPS;
   uint64_t* tfull = empty + OPS;   // [2]
@@ -438,13 +442,16 @@ __global__ void __launch_bounds__(T_THREADS, 1)
       for (int j = 0; j < NX; ++j, ++g) {
         const int s = g % XS;
         tc::mbar_wait(&xempty[s], ((g / XS) & 1) ^ 1);
-        tc::mbar_expect_tx(&xfull[s], XBYTES);
+        tc::mbar_expect_tx(&xfull[s], XBYTES + (args.objective_only ? 0 : MBYTES));
         int c0, c1, c2;
         x_coords<N>(args, t, j, c0, c1, c2);
-        if (args.rows_are_p)
+        if (args.rows_are_p) {
           tc::tma_load_3d(xring + s * XBYTES, &tmXo, &xfull[s], c0, c1, c2);
-        else
+          if (!args.objective_only) tc::tma_load_3d(mring + s * (MBYTES / 4), &tmMask, &xfull[s], c0 / 32, c1, c2);
+        } else {
           tc::tma_load_2d(xring + s * XBYTES, &tmXo, &xfull[s], c0, c1);
+          if (!args.objective_only) tc::tma_load_2d(mring + s * (MBYTES / 4), &tmMask, &xfull[s], c0 / 32, c1);
+        }
       }
     }
   } else if (warp == 1 && lane == 0) {
@@ -516,15 +523,10 @@ __global__ void __launch_bounds__(T_THREADS, 1)
                      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
                        "=r"(r[7])
                      : "r"(tmem + acc * N + ((uint32_t)(32 * quad) << 16) + col0));
-        uint32_t mw[8];
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          const long long off = rowbase + colstride * (gc0 + q);
-          mw[q] = (row_ok && gc0 + q < args.cols && !args.objective_only) ? __ldg(args.maskbits + (off >> 5)) : 0u;
-        }
         tc::mbar_wait(&xfull[s], (g / XS) & 1);
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
         float* xs = reinterpret_cast<float*>(xring + s * XBYTES);
+        const uint32_t* ms = mring + s * (MBYTES / 4);  // [col][4 words]
         if (row_ok) {
 #pragma unroll
           for (int q = 0; q < 8; ++q) {
@@ -536,9 +538,9 @@ __global__ void __launch_bounds__(T_THREADS, 1)
               const float d = x - c;
               f_c += d * d;
             } else {
-              const long long off = rowbase + colstride * (gc0 + q);
+              const uint32_t mw = ms[(part * 8 + q) * 4 + (row >> 5)];  // warp-uniform word
               float xn;
-              if ((mw[q] >> (off & 31)) & 1u) {
+              if ((mw >> (row & 31)) & 1u) {
                 xn = x;  // observed entries restored bit for bit (solver.py:235-236)
               } else {
                 xn = fmaf(x, args.rho, c) * args.inv_onep;  // solver.py:232-234 (fp32: reciprocal, <= 1 ulp)
@@ -605,11 +607,11 @@ __global__ void __launch_bounds__(T_THREADS, 1)
 template <int N, bool SPLIT>
 int go_tma(const CUtensorMap* maps, const ComposeTmaArgs& a, int grid, cudaStream_t st) {
   constexpr int STAGE = (128 + N) * KB2 * 4 * (SPLIT ? 2 : 1);
-  const int smem = 2 * STAGE + XS * XBYTES + 1024 + 256;
+  const int smem = 2 * STAGE + XS * (XBYTES + MBYTES) + 1024 + 256;
   auto fn = k_compose_tma<N, SPLIT>;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) throw std::runtime_error(std::string("compose_tma smem: ") + cudaGetErrorString(e));
-  fn<<<grid, T_THREADS, smem, st>>>(maps[0], maps[1], maps[2], maps[3], maps[4], maps[5], a);
+  fn<<<grid, T_THREADS, smem, st>>>(maps[0], maps[1], maps[2], maps[3], maps[4], maps[5], maps[6], a);
   e = cudaGetLastError();
   if (e != cudaSuccess) throw std::runtime_error(std::string("compose_tma: ") + cudaGetErrorString(e));
   return grid;
@@ -690,7 +692,7 @@ int launch_compose_tc(const ComposeOperands& op, const float* Xo, const uint32_t
   CUtensorMap mAl = op.a_lo ? tc_make_map_f32(op.a_lo, 2, da, sa, box, true) : mA;
   const bool m_pre = op.m_hi != nullptr && (op.m_lo != nullptr || !split3);
   const bool a_pre = op.a_hi != nullptr && (op.a_lo != nullptr || !split3);
-  CUtensorMap maps[6];
+  CUtensorMap maps[7];
   if (a.rows_are_p) {
     maps[0] = mM; maps[1] = mMl; maps[2] = mA; maps[3] = mAl;
     a.a_pre = m_pre; a.b_pre = a_pre;
@@ -700,7 +702,9 @@ int launch_compose_tc(const ComposeOperands& op, const float* Xo, const uint32_t
   }
   // TMA-ring variant when TMA can describe the X tiles (rows = a contiguous
   // run of 128): rows = i (P == 1), or rows = p inside runs of P (P % 128 == 0)
-  const bool tma_x = (!a.rows_are_p || P % 128 == 0) && !getenv("FCTN_COMPOSE_DIRECT");
+  // (the mask words ride along by TMA too: rows must start on 32-entry words)
+  const bool tma_x = ((!a.rows_are_p && I % 128 == 0) || (a.rows_are_p && P % 128 == 0)) &&
+                     !getenv("FCTN_COMPOSE_DIRECT");
   if (tma_x) {
     ComposeTmaArgs t;
     t.maskbits = maskbits;
@@ -736,11 +740,17 @@ int launch_compose_tc(const ComposeOperands& op, const float* Xo, const uint32_t
       uint32_t bx[3] = {128, XC, 1};
       maps[4] = tc_make_map_f32_plain(Xo, 3, dx, sx, bx);
       maps[5] = tc_make_map_f32_plain(Xn, 3, dx, sx, bx);
+      uint64_t dmk[3] = {(uint64_t)(P / 32), (uint64_t)I, Q}, smk[2] = {(uint64_t)(P / 32) * 4, (uint64_t)(P / 32) * I * 4};
+      uint32_t bmk[3] = {4, XC, 1};
+      maps[6] = tc_make_map_u32_plain(maskbits, 3, dmk, smk, bmk);
     } else {
       uint64_t dx[2] = {(uint64_t)I, (uint64_t)p}, sx[1] = {(uint64_t)I * 4};
       uint32_t bx[2] = {128, XC};
       maps[4] = tc_make_map_f32_plain(Xo, 2, dx, sx, bx);
       maps[5] = tc_make_map_f32_plain(Xn, 2, dx, sx, bx);
+      uint64_t dmk[2] = {(uint64_t)(I / 32), (uint64_t)p}, smk[1] = {(uint64_t)(I / 32) * 4};
+      uint32_t bmk[2] = {4, XC};
+      maps[6] = tc_make_map_u32_plain(maskbits, 2, dmk, smk, bmk);
     }
     if (N % XC != 0) N = (N + XC - 1) / XC * XC;
     switch (N) {
