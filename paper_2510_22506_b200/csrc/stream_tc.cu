@@ -23,6 +23,7 @@
 #include <cuda_runtime.h>
 
 
+#include <cstdlib>
 #include <stdexcept>
 #include <string>
 
@@ -178,6 +179,192 @@ __global__ void __launch_bounds__(192, 1)
   }
 }
 
+// ---------------------------------------------------------------------------
+// 3xTF32 variant with the X operand split into TENSOR MEMORY.
+//
+// The split kernel above is shared-memory-bandwidth bound: per 16 KB X stage
+// the converters read the tile and write hi + lo back (48 KB), and the three
+// MMAs re-read A three times.  Here the converter warps read the landed X
+// tile once, round hi = rn(x), lo = rn(x - hi) and store both rows straight
+// into TMEM (tcgen05.st, one row per thread: lane = row), and the MMAs take A
+// from TMEM (kind::tf32, A K-major in TMEM whatever X's layout in smem):
+//     D[:, 0:2NT]  = A_hi x [B_hi | B_lo]     (one N = 2NT instruction)
+//     D[:, 0:NT]  += A_lo x B_hi
+// so shared memory only carries the TMA writes, one converter read of X and
+// the B reads.  The epilogue sums D[:, c] + D[:, NT + c].
+// TMEM: accumulator 2NT columns + per stage 64 columns (32 hi, 32 lo).
+template <int NT>
+struct TsSmem {
+  static constexpr int B_BYTES = NT * BK * 4;
+  static constexpr int STAGE_BYTES = A_BYTES + 2 * B_BYTES;  // [X raw | B hi | B lo]
+  static constexpr int ACC = 2 * NT;
+  static constexpr int S_SMEM = (200 * 1024) / STAGE_BYTES > 6 ? 6 : (200 * 1024) / STAGE_BYTES;
+  static constexpr int S_TMEM = (512 - ACC) / 64;
+  static constexpr int STAGES = S_SMEM < S_TMEM ? S_SMEM : S_TMEM;
+  static constexpr int TOTAL = STAGES * STAGE_BYTES + 1024 + 256;
+};
+
+template <int NT, bool AMN>
+__global__ void __launch_bounds__(192, 1)
+    k_stream_ts(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmM,
+                const __grid_constant__ CUtensorMap tmMl, float* __restrict__ part, int I, int S, long long nkb_total,
+                long long kb_per_split, int nPB, int b_pre) {
+  using L = TsSmem<NT>;
+  constexpr int STAGES = L::STAGES;
+  static_assert(STAGES >= 2, "stage ring");
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * L::STAGE_BYTES);
+  uint64_t* conv = full + STAGES;
+  uint64_t* empty = conv + STAGES;
+  uint64_t* tmem_full = empty + STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int mtile = blockIdx.x;
+  const long long split = blockIdx.y;
+  const long long kb0 = split * kb_per_split;
+  long long kb1 = kb0 + kb_per_split;
+  if (kb1 > nkb_total) kb1 = nkb_total;
+  const int nkb = (int)(kb1 - kb0);
+
+  if (warp == 0 && lane == 0) {
+    tc::tma_prefetch(&tmX);
+    tc::tma_prefetch(&tmM);
+    for (int s = 0; s < STAGES; ++s) {
+      tc::mbar_init(&full[s], 1);
+      tc::mbar_init(&conv[s], 4);
+      tc::mbar_init(&empty[s], 1);
+    }
+    tc::mbar_init(tmem_full, 1);
+    tc::fence_barrier_init();
+  }
+  if (warp == 1) tc::tmem_alloc<512>(tmem_slot);
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0 && lane == 0) {
+    // ---------------- TMA producer
+    const int i0 = mtile * 128;
+    const uint32_t tx = A_BYTES + L::B_BYTES * (b_pre ? 2 : 1);
+    for (int it = 0; it < nkb; ++it) {
+      const int s = it % STAGES;
+      const uint32_t ph = (it / STAGES) & 1;
+      tc::mbar_wait(&empty[s], ph ^ 1);
+      tc::mbar_expect_tx(&full[s], tx);
+      const long long kb = kb0 + it;
+      uint8_t* a = smem + s * L::STAGE_BYTES;
+      uint8_t* b = a + A_BYTES;
+      if (AMN) {
+        const int q0 = (int)(kb * BK);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) tc::tma_load_2d(a + c * 4096, &tmX, &full[s], i0 + 32 * c, q0);
+        tc::tma_load_2d(b, &tmM, &full[s], q0, 0);
+        if (b_pre) tc::tma_load_2d(b + L::B_BYTES, &tmMl, &full[s], q0, 0);
+      } else {
+        const int pb = (int)(kb % nPB) * BK;
+        const int q = (int)(kb / nPB);
+        tc::tma_load_3d(a, &tmX, &full[s], pb, i0, q);
+        tc::tma_load_3d(b, &tmM, &full[s], pb, q, 0);
+        if (b_pre) tc::tma_load_3d(b + L::B_BYTES, &tmMl, &full[s], pb, q, 0);
+      }
+    }
+  } else if (warp == 1 && lane == 0) {
+    // ---------------- MMA issuer
+    constexpr uint32_t idesc2 = tc::idesc_tf32(128, 2 * NT, false, false);
+    constexpr uint32_t idesc1 = tc::idesc_tf32(128, NT, false, false);
+    for (int it = 0; it < nkb; ++it) {
+      const int s = it % STAGES;
+      const uint32_t ph = (it / STAGES) & 1;
+      tc::mbar_wait(&conv[s], ph);
+      tc::fence_after_sync();
+      const uint32_t b = tc::smem_u32(smem + s * L::STAGE_BYTES) + A_BYTES;
+      const uint32_t ahi = tmem + L::ACC + 64 * s, alo = ahi + 32;
+#pragma unroll
+      for (int kk = 0; kk < BK / 8; ++kk) {
+        const uint64_t bd = tc::sdesc(b + kk * 32, 16, 1024);  // rows 0..2NT-1 = [B hi | B lo]
+        tc::mma_tf32_ts(tmem, ahi + 8 * kk, bd, idesc2, (it | kk) != 0);
+        tc::mma_tf32_ts(tmem, alo + 8 * kk, bd, idesc1, 1);
+      }
+      tc::mma_commit(&empty[s]);
+    }
+    tc::mma_commit(tmem_full);
+  } else if (warp >= 2) {
+    // ---------------- X split into TMEM (+ B split in smem when not pre-split), then the epilogue
+    const int q = warp & 3;  // TMEM lane quadrant this warp may access
+    const int row = 32 * q + lane;
+    const int ct = threadIdx.x - 64;
+    for (int it = 0; it < nkb; ++it) {
+      const int s = it % STAGES;
+      tc::mbar_wait(&full[s], (it / STAGES) & 1);
+      const uint8_t* a = smem + s * L::STAGE_BYTES;
+      float x[32];
+      if (AMN) {
+        // four 32-row boxes; K row kq holds 32 consecutive rows, 32-B atoms XOR (kq & 3)
+        const float* box = reinterpret_cast<const float*>(a + (row >> 5) * 4096);
+        const int i = row & 31;
+#pragma unroll
+        for (int kq = 0; kq < 32; ++kq) x[kq] = box[kq * 32 + ((((i >> 3) ^ (kq & 3))) << 3) + (i & 7)];
+      } else {
+        // K-major SW128: row r, 16-B chunk c stored at chunk (c ^ (r & 7))
+        const float4* r4 = reinterpret_cast<const float4*>(a + row * 128);
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          const float4 v = r4[c ^ (row & 7)];
+          x[4 * c] = v.x;
+          x[4 * c + 1] = v.y;
+          x[4 * c + 2] = v.z;
+          x[4 * c + 3] = v.w;
+        }
+      }
+      float lo[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const float h = tc::tf32_rn(x[j]);
+        lo[j] = tc::tf32_rn(x[j] - h);
+        x[j] = h;
+      }
+      const uint32_t ta = tmem + ((uint32_t)(32 * q) << 16) + L::ACC + 64 * s;
+      tc::tmem_st32(ta, x);
+      tc::tmem_st32(ta + 32, lo);
+      if (!b_pre) {
+        uint8_t* b = smem + s * L::STAGE_BYTES + A_BYTES;
+        tc::tf32_split_tile<true>(b, b + L::B_BYTES, L::B_BYTES / 4, ct, 128);
+        tc::fence_proxy_async_smem();
+      }
+      tc::tmem_wait_st();
+      tc::fence_before_sync();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&conv[s]);
+    }
+    tc::mbar_wait(tmem_full, 0);
+    tc::fence_after_sync();
+    const long long i = (long long)mtile * 128 + row;
+    float* out = part + split * (long long)I * S;
+#pragma unroll 1
+    for (int c0 = 0; c0 < NT; c0 += 16) {
+      float v[16], w[16];
+      tc::tmem_ld16(tmem + ((uint32_t)(32 * q) << 16) + c0, v);
+      tc::tmem_ld16(tmem + ((uint32_t)(32 * q) << 16) + NT + c0, w);
+      if (i < I) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const int s = c0 + j;
+          if (s < S) out[i + (long long)I * s] = v[j] + w[j];
+        }
+      }
+    }
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  if (warp == 1) {
+    tc::fence_after_sync();
+    tc::tmem_dealloc<512>(tmem);
+  }
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   if (!fn) {
@@ -219,9 +406,33 @@ void go3(const CUtensorMap& mx, const CUtensorMap& mm, const CUtensorMap& mml, b
 }
 
 template <int NT, bool AMN>
+void go_ts(const CUtensorMap& mx, const CUtensorMap& mm, const CUtensorMap& mml, bool b_pre, float* part, int64_t I,
+           int64_t S, const TcStreamPlan& tp, cudaStream_t st) {
+  const int smem = TsSmem<NT>::TOTAL;
+  auto fn = k_stream_ts<NT, AMN>;
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) throw std::runtime_error(std::string("stream_ts smem: ") + cudaGetErrorString(e));
+  dim3 grid((unsigned)tp.n_mtiles, (unsigned)tp.nsplit);
+  fn<<<grid, 192, smem, st>>>(mx, mm, mml, part, (int)I, (int)S, tp.nkb, tp.kb_per_split, (int)tp.npb,
+                              b_pre ? 1 : 0);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) throw std::runtime_error(std::string("stream_ts: ") + cudaGetErrorString(e));
+}
+
+bool use_ts() {
+  static const int v = [] {
+    const char* e = getenv("FCTN_STREAM_SMEM_SPLIT");  // 1: the older smem-split 3xTF32 kernel
+    return (e && e[0] == '1') ? 0 : 1;
+  }();
+  return v != 0;
+}
+
+template <int NT, bool AMN>
 void go(const CUtensorMap& mx, const CUtensorMap& mm, const CUtensorMap& mml, bool b_pre, float* part, int64_t I,
         int64_t S, const TcStreamPlan& tp, cudaStream_t st) {
-  if (tp.split3)
+  if (tp.split3 && use_ts())
+    go_ts<NT, AMN>(mx, mm, mml, b_pre, part, I, S, tp, st);
+  else if (tp.split3)
     go3<NT, AMN, true>(mx, mm, mml, b_pre, part, I, S, tp, st);
   else
     go3<NT, AMN, false>(mx, mm, mml, b_pre, part, I, S, tp, st);

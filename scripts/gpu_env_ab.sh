@@ -6,6 +6,6 @@ i=0
 for e in "$@"; do
   env $e timeout 300 python bench.py --config $CFG --no-cpu-baseline --no-e2e --steps 10 > $OUT/ab_$i.json 2>$OUT/ab_$i.err
   python -c "
-import json; d=json.load(open('$OUT/ab_$i.json')); k=d['kernels']; print('[$e]', 'ms/sweep', d['ms_per_step'], 'compose', k.get('compose',{}).get('ms_per_step'), 'stream', k.get('stream_y',{}).get('ms_per_step'))" || tail -3 $OUT/ab_$i.err
+import json; d=json.load(open('$OUT/ab_$i.json')); k=d['kernels']; print('[$e]', 'ms/sweep', d['ms_per_step'], {n: round(v.get('ms_per_step', 0), 3) for n, v in k.items()})" || tail -3 $OUT/ab_$i.err
   i=$((i+1))
 done
