@@ -204,8 +204,11 @@ struct TsSmem {
   static constexpr int TOTAL = STAGES * STAGE_BYTES + 1024 + 256;
 };
 
+constexpr int TS_CONV_WARPS = 8;
+constexpr int TS_THREADS = 64 + 32 * TS_CONV_WARPS;
+
 template <int NT, bool AMN>
-__global__ void __launch_bounds__(192, 1)
+__global__ void __launch_bounds__(TS_THREADS, 1)
     k_stream_ts(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmM,
                 const __grid_constant__ CUtensorMap tmMl, float* __restrict__ part, int I, int S, long long nkb_total,
                 long long kb_per_split, int nPB, int b_pre) {
@@ -233,7 +236,7 @@ __global__ void __launch_bounds__(192, 1)
     tc::tma_prefetch(&tmM);
     for (int s = 0; s < STAGES; ++s) {
       tc::mbar_init(&full[s], 1);
-      tc::mbar_init(&conv[s], 4);
+      tc::mbar_init(&conv[s], TS_CONV_WARPS);
       tc::mbar_init(&empty[s], 1);
     }
     tc::mbar_init(tmem_full, 1);
@@ -293,45 +296,50 @@ __global__ void __launch_bounds__(192, 1)
     tc::mma_commit(tmem_full);
   } else if (warp >= 2) {
     // ---------------- X split into TMEM (+ B split in smem when not pre-split), then the epilogue
+    // two warps per TMEM lane quadrant, each owning 16 of the stage's 32 K columns
     const int q = warp & 3;  // TMEM lane quadrant this warp may access
+    const int hf = (warp - 2) >> 2;
     const int row = 32 * q + lane;
     const int ct = threadIdx.x - 64;
     for (int it = 0; it < nkb; ++it) {
       const int s = it % STAGES;
       tc::mbar_wait(&full[s], (it / STAGES) & 1);
       const uint8_t* a = smem + s * L::STAGE_BYTES;
-      float x[32];
+      float x[16];
       if (AMN) {
         // four 32-row boxes; K row kq holds 32 consecutive rows, 32-B atoms XOR (kq & 3)
         const float* box = reinterpret_cast<const float*>(a + (row >> 5) * 4096);
         const int i = row & 31;
 #pragma unroll
-        for (int kq = 0; kq < 32; ++kq) x[kq] = box[kq * 32 + ((((i >> 3) ^ (kq & 3))) << 3) + (i & 7)];
+        for (int j = 0; j < 16; ++j) {
+          const int kq = 16 * hf + j;
+          x[j] = box[kq * 32 + ((((i >> 3) ^ (kq & 3))) << 3) + (i & 7)];
+        }
       } else {
         // K-major SW128: row r, 16-B chunk c stored at chunk (c ^ (r & 7))
         const float4* r4 = reinterpret_cast<const float4*>(a + row * 128);
 #pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          const float4 v = r4[c ^ (row & 7)];
+        for (int c = 0; c < 4; ++c) {
+          const float4 v = r4[(4 * hf + c) ^ (row & 7)];
           x[4 * c] = v.x;
           x[4 * c + 1] = v.y;
           x[4 * c + 2] = v.z;
           x[4 * c + 3] = v.w;
         }
       }
-      float lo[32];
+      float lo[16];
 #pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        const float h = tc::tf32_rn(x[j]);
-        lo[j] = tc::tf32_rn(x[j] - h);
+      for (int j = 0; j < 16; ++j) {
+        const float h = tc::tf32_rn_int(x[j]);
+        lo[j] = tc::tf32_rn_int(x[j] - h);
         x[j] = h;
       }
-      const uint32_t ta = tmem + ((uint32_t)(32 * q) << 16) + L::ACC + 64 * s;
-      tc::tmem_st32(ta, x);
-      tc::tmem_st32(ta + 32, lo);
+      const uint32_t ta = tmem + ((uint32_t)(32 * q) << 16) + L::ACC + 64 * s + 16 * hf;
+      tc::tmem_st16(ta, x);
+      tc::tmem_st16(ta + 32, lo);
       if (!b_pre) {
         uint8_t* b = smem + s * L::STAGE_BYTES + A_BYTES;
-        tc::tf32_split_tile<true>(b, b + L::B_BYTES, L::B_BYTES / 4, ct, 128);
+        tc::tf32_split_tile<true>(b, b + L::B_BYTES, L::B_BYTES / 4, ct, 32 * TS_CONV_WARPS);
         tc::fence_proxy_async_smem();
       }
       tc::tmem_wait_st();
@@ -344,7 +352,7 @@ __global__ void __launch_bounds__(192, 1)
     const long long i = (long long)mtile * 128 + row;
     float* out = part + split * (long long)I * S;
 #pragma unroll 1
-    for (int c0 = 0; c0 < NT; c0 += 16) {
+    for (int c0 = 16 * hf; c0 < NT; c0 += 32) {
       float v[16], w[16];
       tc::tmem_ld16(tmem + ((uint32_t)(32 * q) << 16) + c0, v);
       tc::tmem_ld16(tmem + ((uint32_t)(32 * q) << 16) + NT + c0, w);
@@ -413,8 +421,8 @@ void go_ts(const CUtensorMap& mx, const CUtensorMap& mm, const CUtensorMap& mml,
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) throw std::runtime_error(std::string("stream_ts smem: ") + cudaGetErrorString(e));
   dim3 grid((unsigned)tp.n_mtiles, (unsigned)tp.nsplit);
-  fn<<<grid, 192, smem, st>>>(mx, mm, mml, part, (int)I, (int)S, tp.nkb, tp.kb_per_split, (int)tp.npb,
-                              b_pre ? 1 : 0);
+  fn<<<grid, TS_THREADS, smem, st>>>(mx, mm, mml, part, (int)I, (int)S, tp.nkb, tp.kb_per_split, (int)tp.npb,
+                                     b_pre ? 1 : 0);
   e = cudaGetLastError();
   if (e != cudaSuccess) throw std::runtime_error(std::string("stream_ts: ") + cudaGetErrorString(e));
 }
