@@ -321,7 +321,7 @@ __global__ void __launch_bounds__(THREADS, 1)
 constexpr int KB2 = 8;       // K rows per operand stage (one K=8 MMA step)
 constexpr int BOXB = 32 * KB2 * 4;  // bytes of one 32-row MN-major operand box
 constexpr int XC = 32;       // columns per X sub-tile
-constexpr int XS = 9;        // X ring slots
+constexpr int XS_DEFAULT = 9;  // X ring slots
 constexpr int XKEEP = 3;     // TMA stores allowed in flight
 constexpr int T_CONV0 = 3, T_EPI0 = T_CONV0 + CONV_WARPS, T_NWARPS = T_EPI0 + EPI_WARPS;
 constexpr int T_THREADS = 32 * T_NWARPS;
@@ -338,6 +338,7 @@ struct ComposeTmaArgs {
   int a_pre, b_pre;
   float rho, inv_onep;
   int objective_only;
+  int op3d;  // operand maps are 3-D [32, S, extent/32] views: one TMA per operand per stage
 };
 
 template <int N>
@@ -354,7 +355,19 @@ __device__ __forceinline__ void x_coords(const ComposeTmaArgs& a, long long t, i
   }
 }
 
+// shared memory: OPS operand stages + XS X/mask slots + barriers; the
+// operand ring takes whatever the X ring leaves of the 227 KB
+constexpr int T_SMEM_MAX = 232448 - 1024 /*static red[]*/;
+constexpr int T_TAIL = 1024 /*align*/ + 512 /*barriers*/;
 template <int N, bool SPLIT>
+__host__ __device__ constexpr int t_stage() { return (128 + N) * KB2 * 4 * (SPLIT ? 2 : 1); }
+template <int N, bool SPLIT, int XS>
+__host__ __device__ constexpr int t_ops() {
+  constexpr int o = (T_SMEM_MAX - T_TAIL - XS * (XBYTES + MBYTES)) / t_stage<N, SPLIT>();
+  return o > 8 ? 8 : o;
+}
+
+template <int N, bool SPLIT, int XS>
 __global__ void __launch_bounds__(T_THREADS, 1)
     k_compose_tma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmAl,
                   const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUtensorMap tmBl,
@@ -365,7 +378,8 @@ __global__ void __launch_bounds__(T_THREADS, 1)
   constexpr uint32_t A_B = 128u * KB2 * 4u, B_B = (uint32_t)N * KB2 * 4u;
   constexpr uint32_t HI = A_B + B_B;
   constexpr uint32_t STAGE = HI * (SPLIT ? 2 : 1);
-  constexpr int OPS = 2;
+  constexpr int OPS = t_ops<N, SPLIT, XS>();
+  static_assert(OPS >= 2, "operand ring");
   uint8_t* xring = smem + OPS * STAGE;
   uint32_t* mring = reinterpret_cast<uint32_t*>(xring + XS * XBYTES);  // [XS][XC][4] mask words
   uint64_t* full = reinterpret_cast<uint64_t*>(xring + XS * (XBYTES + MBYTES));
@@ -421,18 +435,25 @@ __global__ void __launch_bounds__(T_THREADS, 1)
         tc::mbar_wait(&empty[s], ((g / OPS) & 1) ^ 1);
         tc::mbar_expect_tx(&full[s], tx);
         uint8_t* st = smem + s * STAGE;
+        if (args.op3d) {  // box [32 rows, KB2, chunks] lands as chunk-major 1 KB boxes
+          tc::tma_load_3d(st, &tmA, &full[s], 0, kb * KB2, r0 / 32);
+          tc::tma_load_3d(st + A_B, &tmB, &full[s], 0, kb * KB2, c0 / 32);
+          if (SPLIT && args.a_pre) tc::tma_load_3d(st + HI, &tmAl, &full[s], 0, kb * KB2, r0 / 32);
+          if (SPLIT && args.b_pre) tc::tma_load_3d(st + HI + A_B, &tmBl, &full[s], 0, kb * KB2, c0 / 32);
+        } else {
 #pragma unroll
-        for (int c = 0; c < 4; ++c) tc::tma_load_2d(st + c * BOXB, &tmA, &full[s], r0 + 32 * c, kb * KB2);
-#pragma unroll
-        for (int c = 0; c < N / 32; ++c)
-          tc::tma_load_2d(st + A_B + c * BOXB, &tmB, &full[s], c0 + 32 * c, kb * KB2);
-        if (SPLIT && args.a_pre)
-#pragma unroll
-          for (int c = 0; c < 4; ++c) tc::tma_load_2d(st + HI + c * BOXB, &tmAl, &full[s], r0 + 32 * c, kb * KB2);
-        if (SPLIT && args.b_pre)
+          for (int c = 0; c < 4; ++c) tc::tma_load_2d(st + c * BOXB, &tmA, &full[s], r0 + 32 * c, kb * KB2);
 #pragma unroll
           for (int c = 0; c < N / 32; ++c)
-            tc::tma_load_2d(st + HI + A_B + c * BOXB, &tmBl, &full[s], c0 + 32 * c, kb * KB2);
+            tc::tma_load_2d(st + A_B + c * BOXB, &tmB, &full[s], c0 + 32 * c, kb * KB2);
+          if (SPLIT && args.a_pre)
+#pragma unroll
+            for (int c = 0; c < 4; ++c) tc::tma_load_2d(st + HI + c * BOXB, &tmAl, &full[s], r0 + 32 * c, kb * KB2);
+          if (SPLIT && args.b_pre)
+#pragma unroll
+            for (int c = 0; c < N / 32; ++c)
+              tc::tma_load_2d(st + HI + A_B + c * BOXB, &tmBl, &full[s], c0 + 32 * c, kb * KB2);
+        }
       }
     }
   } else if (warp == 2 && lane == 0) {
@@ -567,8 +588,9 @@ __global__ void __launch_bounds__(T_THREADS, 1)
               tc::tma_store_2d(&tmXn, xs, c0, c1);
           }
           tc::bulk_commit();
-          tc::bulk_wait_read<XKEEP>();
-          if (g >= XKEEP) tc::mbar_arrive(&xempty[(g - XKEEP) % XS]);
+          constexpr int XK = XS >= 7 ? XKEEP : 2;
+          tc::bulk_wait_read<XK>();
+          if (g >= XK) tc::mbar_arrive(&xempty[(g - XK) % XS]);
         }
       }
       s_d += (double)f_d;
@@ -604,17 +626,34 @@ __global__ void __launch_bounds__(T_THREADS, 1)
   }
 }
 
-template <int N, bool SPLIT>
-int go_tma(const CUtensorMap* maps, const ComposeTmaArgs& a, int grid, cudaStream_t st) {
-  constexpr int STAGE = (128 + N) * KB2 * 4 * (SPLIT ? 2 : 1);
-  const int smem = 2 * STAGE + XS * (XBYTES + MBYTES) + 1024 + 256;
-  auto fn = k_compose_tma<N, SPLIT>;
+template <int N, bool SPLIT, int XS>
+int go_tma_xs(const CUtensorMap* maps, const ComposeTmaArgs& a, int grid, cudaStream_t st) {
+  const int smem = t_ops<N, SPLIT, XS>() * t_stage<N, SPLIT>() + XS * (XBYTES + MBYTES) + T_TAIL;
+  auto fn = k_compose_tma<N, SPLIT, XS>;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) throw std::runtime_error(std::string("compose_tma smem: ") + cudaGetErrorString(e));
   fn<<<grid, T_THREADS, smem, st>>>(maps[0], maps[1], maps[2], maps[3], maps[4], maps[5], maps[6], a);
   e = cudaGetLastError();
   if (e != cudaSuccess) throw std::runtime_error(std::string("compose_tma: ") + cudaGetErrorString(e));
   return grid;
+}
+
+int compose_xs() {
+  static const int v = [] {
+    const char* e = getenv("FCTN_COMPOSE_XS");
+    const int x = e ? atoi(e) : XS_DEFAULT;
+    return (x == 5 || x == 7) ? x : 9;
+  }();
+  return v;
+}
+
+template <int N, bool SPLIT>
+int go_tma(const CUtensorMap* maps, const ComposeTmaArgs& a, int grid, cudaStream_t st) {
+  switch (compose_xs()) {
+    case 5: return go_tma_xs<N, SPLIT, 5>(maps, a, grid, st);
+    case 7: return go_tma_xs<N, SPLIT, 7>(maps, a, grid, st);
+    default: return go_tma_xs<N, SPLIT, 9>(maps, a, grid, st);
+  }
 }
 
 template <int N, bool SPLIT>
@@ -723,12 +762,25 @@ int launch_compose_tc(const ComposeOperands& op, const float* Xo, const uint32_t
     t.rho = a.rho;
     t.inv_onep = a.inv_onep;
     t.objective_only = a.objective_only;
-    uint32_t box16[2] = {32, KB2};
-    // operand maps with 16-row K boxes
-    CUtensorMap tM = tc_make_map_f32(Mh, 2, dm, sm_, box16, true);
-    CUtensorMap tMl = op.m_lo ? tc_make_map_f32(op.m_lo, 2, dm, sm_, box16, true) : tM;
-    CUtensorMap tA = tc_make_map_f32(Ah, 2, da, sa, box16, true);
-    CUtensorMap tAl = op.a_lo ? tc_make_map_f32(op.a_lo, 2, da, sa, box16, true) : tA;
+    if (N % XC != 0) N = (N + XC - 1) / XC * XC;
+    // operand maps with KB2-row K boxes; when both extents are multiples of 32
+    // a 3-D view [32, S, extent / 32] fetches a whole stage operand in one TMA
+    t.op3d = (p % 32 == 0 && I % 32 == 0 && !getenv("FCTN_COMPOSE_OP2D")) ? 1 : 0;
+    const uint32_t nb_m = a.rows_are_p ? 4u : (uint32_t)(N / 32), nb_a = a.rows_are_p ? (uint32_t)(N / 32) : 4u;
+    auto mk = [&](const float* base, int64_t ext, uint32_t nb) {
+      if (t.op3d) {
+        uint64_t d[3] = {32, (uint64_t)S, (uint64_t)(ext / 32)}, sd[2] = {(uint64_t)ext * 4, 128};
+        uint32_t b[3] = {32, KB2, nb};
+        return tc_make_map_f32(base, 3, d, sd, b, true);
+      }
+      uint64_t d[2] = {(uint64_t)ext, (uint64_t)S}, sd[1] = {(uint64_t)ext * 4};
+      uint32_t b[2] = {32, KB2};
+      return tc_make_map_f32(base, 2, d, sd, b, true);
+    };
+    CUtensorMap tM = mk(Mh, p, nb_m);
+    CUtensorMap tMl = op.m_lo ? mk(op.m_lo, p, nb_m) : tM;
+    CUtensorMap tA = mk(Ah, I, nb_a);
+    CUtensorMap tAl = op.a_lo ? mk(op.a_lo, I, nb_a) : tA;
     if (a.rows_are_p) {
       maps[0] = tM; maps[1] = tMl; maps[2] = tA; maps[3] = tAl;
     } else {
