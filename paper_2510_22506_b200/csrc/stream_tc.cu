@@ -211,7 +211,7 @@ template <int NT, bool AMN>
 __global__ void __launch_bounds__(TS_THREADS, 1)
     k_stream_ts(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmM,
                 const __grid_constant__ CUtensorMap tmMl, float* __restrict__ part, int I, int S, long long nkb_total,
-                long long kb_per_split, int nPB, int b_pre) {
+                long long kb_per_split, int nPB, int b_pre, int x3d) {
   using L = TsSmem<NT>;
   constexpr int STAGES = L::STAGES;
   static_assert(STAGES >= 2, "stage ring");
@@ -262,8 +262,12 @@ __global__ void __launch_bounds__(TS_THREADS, 1)
       uint8_t* b = a + A_BYTES;
       if (AMN) {
         const int q0 = (int)(kb * BK);
+        if (x3d) {  // [32, Q, I/32] view: the four 32-row boxes in one TMA
+          tc::tma_load_3d(a, &tmX, &full[s], 0, q0, i0 / 32);
+        } else {
 #pragma unroll
-        for (int c = 0; c < 4; ++c) tc::tma_load_2d(a + c * 4096, &tmX, &full[s], i0 + 32 * c, q0);
+          for (int c = 0; c < 4; ++c) tc::tma_load_2d(a + c * 4096, &tmX, &full[s], i0 + 32 * c, q0);
+        }
         tc::tma_load_2d(b, &tmM, &full[s], q0, 0);
         if (b_pre) tc::tma_load_2d(b + L::B_BYTES, &tmMl, &full[s], q0, 0);
       } else {
@@ -414,15 +418,15 @@ void go3(const CUtensorMap& mx, const CUtensorMap& mm, const CUtensorMap& mml, b
 }
 
 template <int NT, bool AMN>
-void go_ts(const CUtensorMap& mx, const CUtensorMap& mm, const CUtensorMap& mml, bool b_pre, float* part, int64_t I,
-           int64_t S, const TcStreamPlan& tp, cudaStream_t st) {
+void go_ts(const CUtensorMap& mx, const CUtensorMap& mm, const CUtensorMap& mml, bool b_pre, bool x3d, float* part,
+           int64_t I, int64_t S, const TcStreamPlan& tp, cudaStream_t st) {
   const int smem = TsSmem<NT>::TOTAL;
   auto fn = k_stream_ts<NT, AMN>;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) throw std::runtime_error(std::string("stream_ts smem: ") + cudaGetErrorString(e));
   dim3 grid((unsigned)tp.n_mtiles, (unsigned)tp.nsplit);
   fn<<<grid, TS_THREADS, smem, st>>>(mx, mm, mml, part, (int)I, (int)S, tp.nkb, tp.kb_per_split, (int)tp.npb,
-                                     b_pre ? 1 : 0);
+                                     b_pre ? 1 : 0, x3d ? 1 : 0);
   e = cudaGetLastError();
   if (e != cudaSuccess) throw std::runtime_error(std::string("stream_ts: ") + cudaGetErrorString(e));
 }
@@ -436,10 +440,10 @@ bool use_ts() {
 }
 
 template <int NT, bool AMN>
-void go(const CUtensorMap& mx, const CUtensorMap& mm, const CUtensorMap& mml, bool b_pre, float* part, int64_t I,
-        int64_t S, const TcStreamPlan& tp, cudaStream_t st) {
+void go(const CUtensorMap& mx, const CUtensorMap& mx3, const CUtensorMap& mm, const CUtensorMap& mml, bool b_pre,
+        bool x3d, float* part, int64_t I, int64_t S, const TcStreamPlan& tp, cudaStream_t st) {
   if (tp.split3 && use_ts())
-    go_ts<NT, AMN>(mx, mm, mml, b_pre, part, I, S, tp, st);
+    go_ts<NT, AMN>(x3d ? mx3 : mx, mm, mml, b_pre, x3d, part, I, S, tp, st);
   else if (tp.split3)
     go3<NT, AMN, true>(mx, mm, mml, b_pre, part, I, S, tp, st);
   else
@@ -488,12 +492,19 @@ TcStreamPlan plan_stream_tc(int64_t I, int64_t P, int64_t Q, int64_t S, int n_sm
 
 void launch_stream_tc(const float* X, const float* M, float* part, int64_t I, int64_t P, int64_t Q, int64_t S,
                       const TcStreamPlan& tp, cudaStream_t st, const float* Mlo) {
-  CUtensorMap mx, mm, mml;
+  CUtensorMap mx, mx3, mm, mml;
   const bool b_pre = Mlo != nullptr && tp.split3;
+  const bool x3d = P == 1 && I % 32 == 0;
   if (P == 1) {
     uint64_t dx[2] = {(uint64_t)I, (uint64_t)Q}, sx[1] = {(uint64_t)I * 4};
     uint32_t bx[2] = {32, 32};
     mx = make_map(X, 2, dx, sx, bx, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);  // MN-major tf32: 32-B atoms
+    mx3 = mx;
+    if (x3d) {
+      uint64_t d3[3] = {32, (uint64_t)Q, (uint64_t)(I / 32)}, s3[2] = {(uint64_t)I * 4, 128};
+      uint32_t b3[3] = {32, 32, 4};
+      mx3 = make_map(X, 3, d3, s3, b3, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+    }
     uint64_t dm[2] = {(uint64_t)Q, (uint64_t)S}, sm[1] = {(uint64_t)Q * 4};
     uint32_t bm[2] = {32, (uint32_t)tp.nt};
     mm = make_map(M, 2, dm, sm, bm);
@@ -502,6 +513,7 @@ void launch_stream_tc(const float* X, const float* M, float* part, int64_t I, in
     uint64_t dx[3] = {(uint64_t)P, (uint64_t)I, (uint64_t)Q}, sx[2] = {(uint64_t)P * 4, (uint64_t)P * I * 4};
     uint32_t bx[3] = {32, 128, 1};
     mx = make_map(X, 3, dx, sx, bx);
+    mx3 = mx;
     uint64_t dm[3] = {(uint64_t)P, (uint64_t)Q, (uint64_t)S}, sm[2] = {(uint64_t)P * 4, (uint64_t)P * Q * 4};
     uint32_t bm[3] = {32, 1, (uint32_t)tp.nt};
     mm = make_map(M, 3, dm, sm, bm);
@@ -509,10 +521,10 @@ void launch_stream_tc(const float* X, const float* M, float* part, int64_t I, in
   }
   const bool amn = P == 1;
   switch (tp.nt) {
-    case 32: amn ? go<32, true>(mx, mm, mml, b_pre, part, I, S, tp, st) : go<32, false>(mx, mm, mml, b_pre, part, I, S, tp, st); break;
-    case 64: amn ? go<64, true>(mx, mm, mml, b_pre, part, I, S, tp, st) : go<64, false>(mx, mm, mml, b_pre, part, I, S, tp, st); break;
-    case 96: amn ? go<96, true>(mx, mm, mml, b_pre, part, I, S, tp, st) : go<96, false>(mx, mm, mml, b_pre, part, I, S, tp, st); break;
-    default: amn ? go<128, true>(mx, mm, mml, b_pre, part, I, S, tp, st) : go<128, false>(mx, mm, mml, b_pre, part, I, S, tp, st); break;
+    case 32: amn ? go<32, true>(mx, mx3, mm, mml, b_pre, x3d, part, I, S, tp, st) : go<32, false>(mx, mx3, mm, mml, b_pre, x3d, part, I, S, tp, st); break;
+    case 64: amn ? go<64, true>(mx, mx3, mm, mml, b_pre, x3d, part, I, S, tp, st) : go<64, false>(mx, mx3, mm, mml, b_pre, x3d, part, I, S, tp, st); break;
+    case 96: amn ? go<96, true>(mx, mx3, mm, mml, b_pre, x3d, part, I, S, tp, st) : go<96, false>(mx, mx3, mm, mml, b_pre, x3d, part, I, S, tp, st); break;
+    default: amn ? go<128, true>(mx, mx3, mm, mml, b_pre, x3d, part, I, S, tp, st) : go<128, false>(mx, mx3, mm, mml, b_pre, x3d, part, I, S, tp, st); break;
   }
 }
 
