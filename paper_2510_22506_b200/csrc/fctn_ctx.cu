@@ -127,13 +127,13 @@ class Ctx : public Executor {
   int64_t cscratch_cap = 0;
   bool configured = false;
   bool uploaded = false;
-  // N = 3 schedule (see compute_z0): Z_0 = X x_0 A_(0) and its A_0 version
-  void* Zbuf = nullptr;
+  // N = 3 schedule (see compute_z): Z_j = X x_j A_(j) and the A_j version it used
+  void* Zb[3] = {nullptr, nullptr, nullptr};
+  int64_t zver[3] = {-1, -1, -1};
   void* presplit = nullptr;     // fp32 [A hi | A lo | M hi | M lo] for the TC compose
   int64_t presplit_m_cap = 0;   // largest M_k (entries) that is pre-split
   int64_t max_is_ = 0;          // largest factor unfolding (entries), presplit layout
   int64_t ypart_cap = 0;        // doubles in ypart
-  int64_t z_version = -1;
   int mbuf_holds = -1;   // mode whose M_k currently sits in Mbuf (-1: none)
   bool zroute = true;    // FCTN_NO_ZROUTE=1 disables
   // Three-mode sweeps have no data-dependent host decisions and no allocations,
@@ -355,10 +355,10 @@ class Ctx : public Executor {
     }
     A64.clear();
     Ac.clear();
-    for (auto* p : {Ascratch, (double*)Mbuf, (double*)Zbuf, (double*)presplit, (double*)Aslab, yloc, gbuf, Y, G, Fr,
-                     Fi, ypart, partials, epart, colstats, gnet[0], gnet[1]})
+    for (auto* p : {Ascratch, (double*)Mbuf, (double*)Zb[0], (double*)Zb[1], (double*)Zb[2], (double*)presplit,
+                     (double*)Aslab, yloc, gbuf, Y, G, Fr, Fi, ypart, partials, epart, colstats, gnet[0], gnet[1]})
       cudaFree(p);
-    Zbuf = nullptr;
+    Zb[0] = Zb[1] = Zb[2] = nullptr;
     Aslab = nullptr;
     yloc = gbuf = nullptr;
     presplit = nullptr;
@@ -471,8 +471,10 @@ class Ctx : public Executor {
       presplit_m_cap = std::min<int64_t>(max_m, T / 4);
       CK(cudaMalloc(&presplit, (2 * max_is + 2 * presplit_m_cap) * sizeof(float)));
     }
-    if (n == 3) CK(cudaMalloc(&Zbuf, std::max<int64_t>(1, sh.s_of(0) * (T / sh.dims[0])) * esize));
-    z_version = -1;
+    if (n == 3)
+      for (int j = 0; j < 3; ++j)
+        if (j == 0 || 4 * zsize(j) <= T) CK(cudaMalloc(&Zb[j], std::max<int64_t>(1, zsize(j)) * esize));
+    z_invalidate();
     mbuf_holds = -1;
     CK(cudaMalloc(&Y, max_is * sizeof(double)));
     CK(cudaMalloc(&G, max_ss * sizeof(double)));
@@ -741,81 +743,153 @@ class Ctx : public Executor {
   // For three modes the reference's reuse cache never stores anything
   // (network.py:436-438,473) and M_k of a short mode is as large as X
   // (c4: M_2 is 268 M entries).  There Y_k is formed without M_k:
-  //   Z_0 = X x_0 A_(0)  (one tensor-core pass over X, contracting the
-  //                       contiguous mode; T s_0 / I_0 entries),
-  //   Y_k = Z_0 (*) A_(l) (a small contraction over i_l and the bond (0,l)),
-  // the same sums as X_(k) M_k^T in another association.  Z_0 stays valid
-  // while A_0 and X are unchanged, so in orders where mode 0 comes first both
-  // other updates share one pass over X.  The FLOP / cache counters still
-  // come from the planner's replay of the reference chain.
-  bool z_route(int k) const {
-    if (sh.n != 3 || k == 0 || !zroute || !Zbuf) return false;
-    {
-      const int64_t R01 = sh.tri[sh.tri_index(0, 1)], R02 = sh.tri[sh.tri_index(0, 2)];
-      const int64_t R12 = sh.tri[sh.tri_index(1, 2)];
-      if (k == 2 && !(R01 == R12 && R01 <= 8)) return false;
-      if (R12 > 16) return false;
-      if (k == 1 && R02 * sh.dims[1] * R01 * R12 > ypart_cap) return false;
+  //   Z_j = X x_j A_(j)   (one tensor-core pass over X contracting mode j;
+  //                        T s_j / I_j entries),
+  //   Y_k = Z_j (*) A_(l) (a small contraction over i_l and the bond (j, l),
+  //                        l the third mode),
+  // the same sums as X_(k) M_k^T in another association.  Z_j stays valid
+  // while A_j and X are unchanged, so the sweep plans which Z to build so that
+  // each one serves two consecutive updates: two passes over X per sweep for
+  // the three products whatever the visiting order.  The FLOP / cache
+  // counters still come from the planner's replay of the reference chain.
+  int64_t zsize(int j) const { return sh.s_of(j) * (sh.total() / sh.dims[j]); }
+  void z_invalidate() { zver[0] = zver[1] = zver[2] = -1; }
+  // can Z_j be built on this path?
+  bool z_buildable(int j) const {
+    if (sh.n != 3 || !zroute || !Zb[j]) return false;
+    const int64_t T = sh.total();
+    if (dtype == FCTN_F64) return j == 0;
+    if (!use_tc) return false;
+    if (j == 0) return tc_stream_supported(T / sh.dims[0], sh.dims[0], 1, sh.s_of(0));
+    if (!split3) return false;
+    if (j == 1) return tc_stream_batched_supported(sh.dims[0], sh.dims[1], sh.dims[2], sh.s_of(1));
+    return tc_stream_supported(sh.dims[0] * sh.dims[1], 1, sh.dims[2], sh.s_of(2));
+  }
+  int64_t bond_stride(int m, int partner) const {  // in A_(m)'s bond columns
+    int64_t st_ = 1;
+    for (int b : sh.bonds_of(m)) {
+      if (b == sh.bond_label(m, partner)) return st_;
+      st_ *= sh.extent(b);
     }
-    if (dtype == FCTN_F32 && !(use_tc && tc_stream_supported(sh.total() / sh.dims[0], sh.dims[0], 1, sh.s_of(0))))
-      return false;
-    if (z_version == planner->versions[0]) return true;  // fresh: no pass over X at all
-    const int64_t T = sh.total();
-    const int64_t mk = sh.s_of(k) * (T / sh.dims[k]);
-    const int64_t z0 = sh.s_of(0) * (T / sh.dims[0]);
-    return 4 * z0 <= mk;
+    return 0;
   }
-  std::vector<int> z_labels() const {
-    std::vector<int> out;
-    for (int j = 1; j < sh.n; ++j) out.push_back(j);
-    for (int b : sh.bonds_of(0)) out.push_back(b);
-    return out;
+  YzArgs yz_args(int j, int k) const {
+    const int l = 3 - j - k;
+    const int lo = std::min(k, l), hi = std::max(k, l);
+    YzArgs a;
+    a.long_l = (l == lo);
+    a.Ir = sh.dims[lo];
+    a.Io = sh.dims[hi];
+    a.Rc = (int)sh.tri[sh.tri_index(j, l)];
+    a.Rz = (int)sh.tri[sh.tri_index(j, k)];
+    a.Ra = (int)sh.tri[sh.tri_index(k, l)];
+    a.zc = bond_stride(j, l);
+    a.zk = bond_stride(j, k);
+    a.ac = bond_stride(l, j);
+    a.aa = bond_stride(l, k);
+    a.yz = bond_stride(k, j);
+    a.ya = bond_stride(k, l);
+    return a;
   }
-  void compute_z0() {
+  bool yz_ok(int j, int k) const {
+    if (j == k || !z_buildable(j)) return false;
+    const YzArgs a = yz_args(j, k);
+    if (a.long_l) return a.Rc == a.Ra && a.Rc <= 8;
+    return a.Ra <= 16 && (int64_t)a.Rc * a.Ir * a.Rz * a.Ra <= ypart_cap;
+  }
+  // route of each update in `order`: the j whose Z_j forms Y_k, -1 for the M_k stream
+  std::vector<int> plan_routes(const std::vector<int>& order) const {
+    std::vector<int> route(order.size(), -1);
+    if (sh.n != 3 || !zroute) return route;
     const int64_t T = sh.total();
-    const int64_t I0 = sh.dims[0], p0 = T / I0, S0 = sh.s_of(0);
+    int valid = -1;
+    for (size_t t = 0; t < order.size(); ++t) {
+      const int k = order[t];
+      if (valid >= 0 && yz_ok(valid, k)) {
+        route[t] = valid;
+        continue;
+      }
+      const int next = t + 1 < order.size() ? order[t + 1] : -1;
+      int best = -1;
+      bool best_next = false;
+      for (int j = 0; j < 3; ++j) {
+        if (!yz_ok(j, k)) continue;
+        const bool serves = next >= 0 && yz_ok(j, next);
+        if (best < 0 || (serves && !best_next) || (serves == best_next && zsize(j) < zsize(best))) {
+          best = j;
+          best_next = serves;
+        }
+      }
+      if (best >= 0 && !best_next) {
+        // a Z for this update alone: keep the M_k stream when M_k is the cheaper operand
+        const int64_t mk = sh.s_of(k) * (T / sh.dims[k]);
+        const bool z_wins = dtype == FCTN_F64 ? 4 * zsize(best) <= mk : 2 * zsize(best) <= 3 * mk;
+        if (!z_wins) best = -1;
+      }
+      route[t] = best;
+      valid = best;
+    }
+    return route;
+  }
+  void compute_z(int j) {
+    const int64_t T = sh.total();
+    const int64_t Ij = sh.dims[j], pj = T / Ij, Sj = sh.s_of(j);
     int pm = pbegin(FCTN_K_ZPASS);
     if (dtype == FCTN_F32) {
-      // the stream kernel with the roles of the modes swapped: rows = (i1, i2),
-      // K = i0 (X's contiguous mode, K-major tiles), B = A_(0)
-      TcStreamPlan tp = plan_stream_tc(p0, I0, 1, S0, n_sm, split3);
-      tp.kb_per_split = tp.nkb;
-      tp.nsplit = 1;
-      const float* bh = (const float*)fac_ptr(0);
+      const float* bh = (const float*)fac_ptr(j);
       const float* bl = nullptr;
-      if (split3) {  // A_(0) is tiny: split it once in HBM
+      if (split3) {  // A_(j) is tiny: split it once in HBM
         float* h = (float*)presplit;
-        launch_tf32_split(bh, h, h + max_is_, I0 * S0, st);
+        launch_tf32_split(bh, h, h + max_is_, Ij * Sj, st);
         bh = h;
         bl = h + max_is_;
         ++launches;
       }
-      launch_stream_tc((const float*)X[cur], bh, (float*)Zbuf, p0, I0, 1, S0, tp, st, bl);
+      if (j == 0) {
+        // the stream kernel with the roles of the modes swapped: rows = (i1, i2),
+        // K = i0 (X's contiguous mode, K-major tiles), B = A_(0)
+        TcStreamPlan tp = plan_stream_tc(pj, Ij, 1, Sj, n_sm, split3);
+        tp.kb_per_split = tp.nkb;
+        tp.nsplit = 1;
+        launch_stream_tc((const float*)X[cur], bh, (float*)Zb[0], pj, Ij, 1, Sj, tp, st, bl);
+      } else if (j == 1) {
+        // a batch over i2 of MN-major [i0 x i1] x A_(1) products
+        launch_stream_tc_batched((const float*)X[cur], bh, bl, (float*)Zb[1], sh.dims[0], sh.dims[1], sh.dims[2], Sj,
+                                 n_sm, st);
+      } else {
+        // rows = (i0, i1) contiguous, K = i2: the k = 0 stream shape with B = A_(2)
+        TcStreamPlan tp = plan_stream_tc(pj, 1, Ij, Sj, n_sm, split3);
+        tp.kb_per_split = tp.nkb;
+        tp.nsplit = 1;
+        launch_stream_tc((const float*)X[cur], bh, (float*)Zb[2], pj, 1, Ij, Sj, tp, st, bl);
+      }
     } else {
-      StreamPlan sp = plan_stream(p0, S0, I0, target_ctas());
-      launch_stream<double>((const double*)X[cur], (const double*)fac_ptr(0), ypart, p0, I0, S0, I0, sp, st);
-      launch_reduce_splits(ypart, sp.nsplit, p0 * S0, nullptr, 0.0, (double*)Zbuf, st);
+      StreamPlan sp = plan_stream(pj, Sj, Ij, target_ctas());
+      launch_stream<double>((const double*)X[cur], (const double*)fac_ptr(0), ypart, pj, Ij, Sj, Ij, sp, st);
+      launch_reduce_splits(ypart, sp.nsplit, pj * Sj, nullptr, 0.0, (double*)Zb[0], st);
       ++launches;
     }
     ++launches;
-    pend(pm, (double)esize * (T + I0 * S0 + p0 * S0), 1);
-    z_version = planner->versions[0];
+    pend(pm, (double)esize * (T + Ij * Sj + pj * Sj), 1);
+    zver[j] = planner->versions[j];
   }
-  void y_from_z(int k) {
-    const int l = (k == 1) ? 2 : 1;
+  void y_from_z(int j, int k) {
+    const int l = 3 - j - k;
     const int64_t I = sh.dims[k], S = sh.s_of(k);
-    const int R01 = (int)sh.tri[sh.tri_index(0, 1)], R02 = (int)sh.tri[sh.tri_index(0, 2)];
-    const int R12 = (int)sh.tri[sh.tri_index(1, 2)];
+    const YzArgs a = yz_args(j, k);
+    // sharded: Y_0 rows are this slab's (all-gathered), other Y_k are this slab's share (all-reduced)
+    double* yout = (sharded() && k == 0) ? yloc : Y;
     int pm = pbegin(FCTN_K_YSMALL);
-    if (dtype == FCTN_F32)
-      launch_y_from_z<float>((const float*)Zbuf, (const float*)Ac[l], k, sh.dims[1], sh.dims[2], R01, R02, R12, Y,
-                             ypart, st);
-    else
-      launch_y_from_z<double>((const double*)Zbuf, A64[l], k, sh.dims[1], sh.dims[2], R01, R02, R12, Y, ypart, st);
-    if (!sharded()) launch_axpy(Y, A64[k], rho, I * S, st);  // + rho A_prev (sylvester.py:106)
-    launches += 2;
-    pend(pm, (double)esize * ((sh.total() / sh.dims[0]) * sh.s_of(0)) + 8.0 * I * S, 2);
-    if (sharded()) finish_y(k, false);  // Z_0 summed over this slab only
+    const int nl = dtype == FCTN_F32
+                       ? launch_y_from_z<float>((const float*)Zb[j], (const float*)fac_ptr(l), a, yout, ypart, st)
+                       : launch_y_from_z<double>((const double*)Zb[j], A64[l], a, yout, ypart, st);
+    launches += nl;
+    if (!sharded()) {
+      launch_axpy(Y, A64[k], rho, I * S, st);  // + rho A_prev (sylvester.py:106)
+      ++launches;
+    }
+    pend(pm, (double)esize * zsize(j) + 8.0 * I * S, nl + (sharded() ? 0 : 1));
+    if (sharded()) finish_y(k, k == 0);
   }
   // M_j of the current factors into Mbuf, outside the reference's chain (no meter)
   void build_m_direct(int k) {
@@ -837,10 +911,10 @@ class Ctx : public Executor {
     mbuf_holds = k;
   }
 
-  void factor_update(int k, int extrap, double alpha, double beta) {
-    if (z_route(k)) {
-      if (z_version != planner->versions[0]) compute_z0();
-      y_from_z(k);
+  void factor_update(int k, int zj, int extrap, double alpha, double beta) {
+    if (zj >= 0) {
+      if (zver[zj] != planner->versions[zj]) compute_z(zj);
+      y_from_z(zj, k);
     } else {
       y_stream(k);
     }
@@ -993,15 +1067,17 @@ class Ctx : public Executor {
   // all device work of one sweep (plus its host bookkeeping)
   void sweep_device(const std::vector<int>& order, int extrap, double alpha, double beta) {
     const int n = sh.n;
-    for (int k : order) {
-      const bool zr = z_route(k);
+    const std::vector<int> route = plan_routes(order);
+    for (size_t t = 0; t < order.size(); ++t) {
+      const int k = order[t];
+      const bool zr = route[t] >= 0;
       if (alg == FCTN_ALG_ACCEL) {
         planner->partial_cached(k, order, zr ? nullptr : this, M_ID);  // dry replay when M_k is not needed
       } else {
         planner->partial_plain(k, zr ? nullptr : this, M_ID);
       }
       mbuf_holds = zr ? -1 : k;
-      factor_update(k, extrap, alpha, beta);
+      factor_update(k, route[t], extrap, alpha, beta);
     }
     int k_last = order.back();
     if (alg == FCTN_ALG_ACCEL) {
@@ -1037,13 +1113,14 @@ class Ctx : public Executor {
   void precapture(int extrap, double alpha, double beta) {
     const Meter meter0 = planner->meter;
     const std::vector<int64_t> versions0 = planner->versions;
-    const int cur0 = cur, zv0 = z_version, mh0 = mbuf_holds;
+    const int cur0 = cur, mh0 = mbuf_holds;
+    int64_t zv0[3] = {zver[0], zver[1], zver[2]};
     const int64_t l0 = launches;
     std::vector<int> order{0, 1, 2};
     for (int parity = 0; parity < 2; ++parity) {
       do {
         cur = parity;
-        z_version = -1;
+        z_invalidate();
         mbuf_holds = -1;
         launches = 0;
         const std::string key = graph_key(order, parity, extrap, alpha, beta);
@@ -1068,7 +1145,7 @@ class Ctx : public Executor {
     planner->meter = meter0;
     planner->versions = versions0;
     cur = cur0;
-    z_version = zv0;
+    for (int j = 0; j < 3; ++j) zver[j] = zv0[j];
     mbuf_holds = mh0;
     launches = l0;
   }
@@ -1142,7 +1219,7 @@ class Ctx : public Executor {
     CK(cudaEventRecord(ev1, st));
     fetch_stats();
     cur ^= 1;
-    z_version = -1;  // X changed
+    z_invalidate();  // X changed
     mbuf_holds = -1;
     float ms = 0.f;
     CK(cudaEventElapsedTime(&ms, ev0, ev1));
@@ -1249,7 +1326,7 @@ int fctn_upload(fctn_ctx* c, const void* x_F, const uint8_t* mask_F) {
     CK(cudaStreamSynchronize(x.st));
     x.cur = 0;
     x.uploaded = true;
-    x.z_version = -1;
+    x.z_invalidate();
     x.mbuf_holds = -1;
   });
 }
@@ -1296,7 +1373,7 @@ int fctn_upload_f64(fctn_ctx* c, const double* x_F, const uint8_t* mask_F) {
     CK(cudaStreamSynchronize(x.st));
     x.cur = 0;
     x.uploaded = true;
-    x.z_version = -1;
+    x.z_invalidate();
     x.mbuf_holds = -1;
   });
 }
@@ -1334,7 +1411,7 @@ int fctn_set_factors(fctn_ctx* c, const double* const* a_unf, const int64_t* ver
     }
     for (int k = 0; k < x.gsh.n; ++k) x.factor_refresh(k);
     x.refresh_slab();
-    x.z_version = -1;
+    x.z_invalidate();
     x.mbuf_holds = -1;
     if (reset_cache) x.planner->reset_cache(&x);
     CK(cudaStreamSynchronize(x.st));

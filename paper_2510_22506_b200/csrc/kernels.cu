@@ -455,121 +455,148 @@ void launch_axpy(double* y, const double* x, double a, int64_t n, cudaStream_t s
   check_launch("axpy");
 }
 
-// N = 3 schedule, Y_k = Z_0 (*) A_(l) with Z_0 = [i1, i2, b01, b02] (i1 fastest):
-//  k = 2: Y[i2, b02, b12] = sum_{i1, b01} Z[i1, i2, b01, b02] A1[i1, b01, b12]
-//         CTA per (b02, group of G i2); a thread keeps A1[i1, :, :] in registers
-//         for its i1 and accumulates G x R12 sums; fixed-order block tree.
-//  k = 1: Y[i1, b01, b12] = sum_{i2, b02} Z[i1, i2, b01, b02] A2[i2, b02, b12]
-//         thread per (i1, b01), CTAs also split b02 (partials reduced in order);
-//         A2 values are warp-uniform.
+// N = 3 schedule, Y_k = Z_j (*) A_(l) (kernels.cuh: YzArgs).
+//  long_l (contract the fast row mode r = i_l):
+//     Y[o, bz, ba] = sum_{r, bc} Z[r, o, bc, bz] A[r, bc, ba]
+//     CTA per (bz, group of G o); a thread keeps A[r, :, :] in registers for
+//     its r and accumulates G x RA sums; fixed-order block tree.
+//  otherwise (contract the slow row mode o = i_l, rows r = i_k):
+//     Y[r, bz, ba] = sum_{o, bc} Z[r, o, bc, bz] A[o, bc, ba]
+//     thread per (r, bz), CTAs also split bc (partials reduced in order);
+//     A values are warp-uniform.
 // fp64 accumulation, deterministic.
-template <typename T, int R01, int R12, int G>
-__global__ void __launch_bounds__(256) k_yz2(const T* __restrict__ Z, const T* __restrict__ A1, int64_t I1,
-                                             int64_t I2, int R02, double* __restrict__ Y) {
-  const int64_t b02 = blockIdx.x % R02, i2_0 = (blockIdx.x / R02) * G;
-  double acc[G][R12];
+template <typename T, int RC, int RA, int G>
+__global__ void __launch_bounds__(256) k_yzl(const T* __restrict__ Z, const T* __restrict__ A, YzArgs p,
+                                             double* __restrict__ Y, int64_t r_chunk) {
+  const int64_t bz = blockIdx.x % p.Rz, o0 = (blockIdx.x / p.Rz) * G;
+  const int64_t rows = p.Ir * p.Io;
+  const int64_t r_lo = blockIdx.y * r_chunk, r_hi = (p.Ir < r_lo + r_chunk) ? p.Ir : r_lo + r_chunk;
+  Y += blockIdx.y * (p.Io * p.Rz * RA);  // this r-split's partial
+  double acc[G][RA];
 #pragma unroll
   for (int g = 0; g < G; ++g)
 #pragma unroll
-    for (int c = 0; c < R12; ++c) acc[g][c] = 0.0;
-  for (int64_t i1 = threadIdx.x; i1 < I1; i1 += 256) {
-    T a[R01][R12];
+    for (int c = 0; c < RA; ++c) acc[g][c] = 0.0;
+  for (int64_t r = r_lo + threadIdx.x; r < r_hi; r += 256) {
+    T a[RC][RA];
 #pragma unroll
-    for (int b = 0; b < R01; ++b)
+    for (int b = 0; b < RC; ++b)
 #pragma unroll
-      for (int c = 0; c < R12; ++c) a[b][c] = A1[i1 + I1 * (b + (int64_t)R01 * c)];
+      for (int c = 0; c < RA; ++c) a[b][c] = A[r + p.Ir * (b * p.ac + c * p.aa)];
 #pragma unroll
     for (int g = 0; g < G; ++g) {
-      const int64_t i2 = i2_0 + g;
-      if (i2 >= I2) break;
+      const int64_t o = o0 + g;
+      if (o >= p.Io) break;
 #pragma unroll
-      for (int b = 0; b < R01; ++b) {
-        const double z = (double)Z[i1 + I1 * (i2 + I2 * (b + (int64_t)R01 * b02))];
+      for (int b = 0; b < RC; ++b) {
+        const double z = (double)Z[r + p.Ir * o + rows * (b * p.zc + bz * p.zk)];
 #pragma unroll
-        for (int c = 0; c < R12; ++c) acc[g][c] += z * (double)a[b][c];
+        for (int c = 0; c < RA; ++c) acc[g][c] += z * (double)a[b][c];
       }
     }
   }
-  __shared__ double red[8][G * R12];
+  __shared__ double red[8][G * RA];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
 #pragma unroll
   for (int g = 0; g < G; ++g)
 #pragma unroll
-    for (int c = 0; c < R12; ++c) {
+    for (int c = 0; c < RA; ++c) {
       double v = acc[g][c];
       for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-      if (lane == 0) red[wid][g * R12 + c] = v;
+      if (lane == 0) red[wid][g * RA + c] = v;
     }
   __syncthreads();
-  for (int e = threadIdx.x; e < G * R12; e += 256) {
-    const int g = e / R12, c = e % R12;
-    const int64_t i2 = i2_0 + g;
-    if (i2 >= I2) continue;
+  for (int e = threadIdx.x; e < G * RA; e += 256) {
+    const int g = e / RA, c = e % RA;
+    const int64_t o = o0 + g;
+    if (o >= p.Io) continue;
     double v = 0.0;
     for (int q = 0; q < 8; ++q) v += red[q][e];
-    Y[i2 + I2 * (b02 + (int64_t)R02 * c)] = v;
+    Y[o + p.Io * (bz * p.yz + c * p.ya)] = v;
   }
 }
 
 template <typename T, int RB>
-__global__ void __launch_bounds__(256) k_yz1(const T* __restrict__ Z, const T* __restrict__ A2, int64_t I1,
-                                             int64_t I2, int R01, int R02, int R12, double* __restrict__ part) {
-  const int64_t i1 = blockIdx.x * 256LL + threadIdx.x;
-  const int b01 = blockIdx.y, b02 = blockIdx.z;
-  if (i1 >= I1) return;
+__global__ void __launch_bounds__(256) k_yzs(const T* __restrict__ Z, const T* __restrict__ A, YzArgs p,
+                                             double* __restrict__ part) {
+  constexpr int OC = 64;  // o values per shared-memory chunk of A
+  __shared__ double as[OC][RB];
+  const int64_t r = blockIdx.x * 256LL + threadIdx.x;
+  const int bz = blockIdx.y, bc = blockIdx.z;
+  const bool live = r < p.Ir;
+  const int64_t rows = p.Ir * p.Io;
+  const T* zp = Z + (live ? r : 0) + rows * (bc * p.zc + bz * p.zk);
+  const T* ap = A + p.Io * (bc * p.ac);
   double acc[RB];
 #pragma unroll
   for (int c = 0; c < RB; ++c) acc[c] = 0.0;
-  for (int64_t i2 = 0; i2 < I2; ++i2) {
-    const double z = (double)Z[i1 + I1 * (i2 + I2 * (b01 + (int64_t)R01 * b02))];
+  for (int64_t o0 = 0; o0 < p.Io; o0 += OC) {
+    const int on = (int)(p.Io - o0 < OC ? p.Io - o0 : OC);
+    __syncthreads();
+    for (int e = threadIdx.x; e < OC * RB; e += 256) {
+      const int o = e % OC, c = e / OC;
+      as[o][c] = (o < on && c < p.Ra) ? (double)ap[o0 + o + p.Io * (c * p.aa)] : 0.0;
+    }
+    __syncthreads();
+    if (live) {
+#pragma unroll 8
+      for (int o = 0; o < on; ++o) {
+        const double z = (double)zp[p.Ir * (o0 + o)];
 #pragma unroll
-    for (int c = 0; c < RB; ++c)
-      if (c < R12) acc[c] += z * (double)__ldg(A2 + i2 + I2 * (b02 + (int64_t)R02 * c));
+        for (int c = 0; c < RB; ++c) acc[c] = fma(z, as[o][c], acc[c]);
+      }
+    }
   }
-  const int64_t n = I1 * R01 * R12;
+  if (!live) return;
+  const int64_t n = p.Ir * p.Rz * p.Ra;
 #pragma unroll
   for (int c = 0; c < RB; ++c)
-    if (c < R12) part[b02 * n + i1 + I1 * (b01 + (int64_t)R01 * c)] = acc[c];
+    if (c < p.Ra) part[bc * n + r + p.Ir * (bz * p.yz + c * p.ya)] = acc[c];
 }
 
-template <typename T, int R01, int R12>
-static void yz2_go(const T* Z, const T* Al, int64_t I1, int64_t I2, int R02, double* Y, cudaStream_t st) {
+template <typename T, int R>
+static int yzl_go(const T* Z, const T* Al, const YzArgs& a, double* Y, double* part, cudaStream_t st) {
   constexpr int G = 8;
-  const unsigned grid = (unsigned)(R02 * ((I2 + G - 1) / G));
-  k_yz2<T, R01, R12, G><<<grid, 256, 0, st>>>(Z, Al, I1, I2, R02, Y);
+  const int64_t nxy = a.Rz * ((a.Io + G - 1) / G);
+  // split the contracted rows so that the grid covers the GPU; partials reduced in order
+  int64_t rs = (4 * 148 + nxy - 1) / nxy;
+  rs = std::max<int64_t>(1, std::min<int64_t>(rs, (a.Ir + 255) / 256));
+  const int64_t chunk = (a.Ir + rs - 1) / rs;
+  rs = (a.Ir + chunk - 1) / chunk;
+  dim3 grid((unsigned)nxy, (unsigned)rs);
+  k_yzl<T, R, R, G><<<grid, 256, 0, st>>>(Z, Al, a, rs > 1 ? part : Y, chunk);
+  if (rs > 1) launch_reduce_splits(part, (int)rs, a.Io * a.Rz * R, nullptr, 0.0, Y, st);
+  return rs > 1 ? 2 : 1;
 }
 
 template <typename T>
-void launch_y_from_z(const T* Z, const T* Al, int k, int64_t I1, int64_t I2, int R01, int R02, int R12, double* Y,
-                     double* part, cudaStream_t st) {
-  if (R12 > 16) throw std::runtime_error("y_from_z: bond > 16");
-  if (k == 2) {
-    if (R01 == R12 && R01 <= 8) {
-      switch (R01) {
-        case 1: yz2_go<T, 1, 1>(Z, Al, I1, I2, R02, Y, st); break;
-        case 2: yz2_go<T, 2, 2>(Z, Al, I1, I2, R02, Y, st); break;
-        case 3: yz2_go<T, 3, 3>(Z, Al, I1, I2, R02, Y, st); break;
-        case 4: yz2_go<T, 4, 4>(Z, Al, I1, I2, R02, Y, st); break;
-        case 5: yz2_go<T, 5, 5>(Z, Al, I1, I2, R02, Y, st); break;
-        case 6: yz2_go<T, 6, 6>(Z, Al, I1, I2, R02, Y, st); break;
-        case 7: yz2_go<T, 7, 7>(Z, Al, I1, I2, R02, Y, st); break;
-        default: yz2_go<T, 8, 8>(Z, Al, I1, I2, R02, Y, st); break;
-      }
-      check_launch("y_from_z2");
-      return;
+int launch_y_from_z(const T* Z, const T* Al, const YzArgs& a, double* Y, double* part, cudaStream_t st) {
+  if (a.long_l) {
+    int nl = 0;
+    if (a.Rc != a.Ra || a.Rc > 8) throw std::runtime_error("y_from_z: non-uniform bonds need the generic contraction");
+    switch (a.Rc) {
+      case 1: nl = yzl_go<T, 1>(Z, Al, a, Y, part, st); break;
+      case 2: nl = yzl_go<T, 2>(Z, Al, a, Y, part, st); break;
+      case 3: nl = yzl_go<T, 3>(Z, Al, a, Y, part, st); break;
+      case 4: nl = yzl_go<T, 4>(Z, Al, a, Y, part, st); break;
+      case 5: nl = yzl_go<T, 5>(Z, Al, a, Y, part, st); break;
+      case 6: nl = yzl_go<T, 6>(Z, Al, a, Y, part, st); break;
+      case 7: nl = yzl_go<T, 7>(Z, Al, a, Y, part, st); break;
+      default: nl = yzl_go<T, 8>(Z, Al, a, Y, part, st); break;
     }
-    throw std::runtime_error("y_from_z: non-uniform bonds need the generic contraction");
+    check_launch("y_from_z_long");
+    return nl;
   }
-  dim3 grid((unsigned)((I1 + 255) / 256), (unsigned)R01, (unsigned)R02);
-  if (R12 <= 8) k_yz1<T, 8><<<grid, 256, 0, st>>>(Z, Al, I1, I2, R01, R02, R12, part);
-  else k_yz1<T, 16><<<grid, 256, 0, st>>>(Z, Al, I1, I2, R01, R02, R12, part);
-  check_launch("y_from_z1");
-  launch_reduce_splits(part, R02, I1 * R01 * R12, nullptr, 0.0, Y, st);
+  if (a.Ra > 16) throw std::runtime_error("y_from_z: bond > 16");
+  dim3 grid((unsigned)((a.Ir + 255) / 256), (unsigned)a.Rz, (unsigned)a.Rc);
+  if (a.Ra <= 8) k_yzs<T, 8><<<grid, 256, 0, st>>>(Z, Al, a, part);
+  else k_yzs<T, 16><<<grid, 256, 0, st>>>(Z, Al, a, part);
+  check_launch("y_from_z_short");
+  launch_reduce_splits(part, a.Rc, a.Ir * a.Rz * a.Ra, nullptr, 0.0, Y, st);
+  return 2;
 }
-template void launch_y_from_z<float>(const float*, const float*, int, int64_t, int64_t, int, int, int, double*,
-                                     double*, cudaStream_t);
-template void launch_y_from_z<double>(const double*, const double*, int, int64_t, int64_t, int, int, int, double*,
-                                      double*, cudaStream_t);
+template int launch_y_from_z<float>(const float*, const float*, const YzArgs&, double*, double*, cudaStream_t);
+template int launch_y_from_z<double>(const double*, const double*, const YzArgs&, double*, double*, cudaStream_t);
 
 __global__ void k_convert(const double* __restrict__ in, float* __restrict__ out, int64_t n) {
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)

@@ -36,10 +36,20 @@ void launch_permute(const T* in, T* out, const PermDesc& d, int64_t numel, cudaS
 
 void launch_convert_f64_f32(const double* in, float* out, int64_t n, cudaStream_t st);
 void launch_convert_f32_f64(const float* in, double* out, int64_t n, cudaStream_t st);
-// N = 3 schedule: Y_k (k = 1, 2) = Z_0 (*) A_(l), Z_0 = [i1, i2, b01, b02]; Y fp64 (I_k x s_k)
+// N = 3 schedule: Y_k = Z_j (*) A_(l) with Z_j = X x_j A_(j) = [r, o, b_j.., b_j..]
+// (rows: the two other modes, the lower one fastest; then the bonds of j in
+// A_(j)'s column order) and l the third mode.  Strides are in units of the
+// row extents: Z bond (j,l) zc, bond (j,k) zk; A_(l) bond (l,j) ac, (l,k) aa;
+// Y_k bond (k,j) yz, (k,l) ya.  long_l: l is the fast row mode (r = i_l,
+// o = i_k), otherwise k is (r = i_k, o = i_l).  Y fp64 (I_k x s_k).
+struct YzArgs {
+  int64_t Ir, Io;
+  int Rc, Rz, Ra;
+  int64_t zc, zk, ac, aa, yz, ya;
+  bool long_l;
+};
 template <typename T>
-void launch_y_from_z(const T* Z, const T* Al, int k, int64_t I1, int64_t I2, int R01, int R02, int R12, double* Y,
-                     double* part, cudaStream_t st);
+int launch_y_from_z(const T* Z, const T* Al, const YzArgs& a, double* Y, double* part, cudaStream_t st);  // launches
 // mode-0 sharding helpers (fctn_set_comm)
 void launch_copy_rows(const double* A, int64_t I, int64_t S, int64_t lo, int64_t rows, void* out, bool f32,
                       cudaStream_t st);
@@ -85,6 +95,9 @@ TcStreamPlan plan_stream_tc(int64_t I, int64_t P, int64_t Q, int64_t S, int n_sm
 // split3 only the streamed X tile is split in shared memory
 void launch_stream_tc(const float* X, const float* M, float* part, int64_t I, int64_t P, int64_t Q, int64_t S,
                       const TcStreamPlan& tp, cudaStream_t st, const float* Mlo = nullptr);
+bool tc_stream_batched_supported(int64_t R, int64_t Q, int64_t NB, int64_t S);
+void launch_stream_tc_batched(const float* X, const float* Bh, const float* Bl, float* out, int64_t R, int64_t Q,
+                              int64_t NB, int64_t S, int n_sm, cudaStream_t st);
 
 // ---------------------------------------------------------------- K3 solve
 struct DftPlan {

@@ -211,7 +211,7 @@ template <int NT, bool AMN>
 __global__ void __launch_bounds__(TS_THREADS, 1)
     k_stream_ts(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmM,
                 const __grid_constant__ CUtensorMap tmMl, float* __restrict__ part, int I, int S, long long nkb_total,
-                long long kb_per_split, int nPB, int b_pre, int x3d) {
+                long long kb_per_split, int nPB, int b_pre, int x3d, int rows_b) {
   using L = TsSmem<NT>;
   constexpr int STAGES = L::STAGES;
   static_assert(STAGES >= 2, "stage ring");
@@ -262,7 +262,9 @@ __global__ void __launch_bounds__(TS_THREADS, 1)
       uint8_t* b = a + A_BYTES;
       if (AMN) {
         const int q0 = (int)(kb * BK);
-        if (x3d) {  // [32, Q, I/32] view: the four 32-row boxes in one TMA
+        if (rows_b) {  // batched [32, Q, rows_b/32, batch] view (tiles never straddle a batch)
+          tc::tma_load_4d(a, &tmX, &full[s], 0, q0, (i0 % rows_b) / 32, i0 / rows_b);
+        } else if (x3d) {  // [32, Q, I/32] view: the four 32-row boxes in one TMA
           tc::tma_load_3d(a, &tmX, &full[s], 0, q0, i0 / 32);
         } else {
 #pragma unroll
@@ -419,14 +421,14 @@ void go3(const CUtensorMap& mx, const CUtensorMap& mm, const CUtensorMap& mml, b
 
 template <int NT, bool AMN>
 void go_ts(const CUtensorMap& mx, const CUtensorMap& mm, const CUtensorMap& mml, bool b_pre, bool x3d, float* part,
-           int64_t I, int64_t S, const TcStreamPlan& tp, cudaStream_t st) {
+           int64_t I, int64_t S, const TcStreamPlan& tp, cudaStream_t st, int rows_b = 0) {
   const int smem = TsSmem<NT>::TOTAL;
   auto fn = k_stream_ts<NT, AMN>;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) throw std::runtime_error(std::string("stream_ts smem: ") + cudaGetErrorString(e));
   dim3 grid((unsigned)tp.n_mtiles, (unsigned)tp.nsplit);
   fn<<<grid, TS_THREADS, smem, st>>>(mx, mm, mml, part, (int)I, (int)S, tp.nkb, tp.kb_per_split, (int)tp.npb,
-                                     b_pre ? 1 : 0, x3d ? 1 : 0);
+                                     b_pre ? 1 : 0, x3d ? 1 : 0, rows_b);
   e = cudaGetLastError();
   if (e != cudaSuccess) throw std::runtime_error(std::string("stream_ts: ") + cudaGetErrorString(e));
 }
@@ -525,6 +527,35 @@ void launch_stream_tc(const float* X, const float* M, float* part, int64_t I, in
     case 64: amn ? go<64, true>(mx, mx3, mm, mml, b_pre, x3d, part, I, S, tp, st) : go<64, false>(mx, mx3, mm, mml, b_pre, x3d, part, I, S, tp, st); break;
     case 96: amn ? go<96, true>(mx, mx3, mm, mml, b_pre, x3d, part, I, S, tp, st) : go<96, false>(mx, mx3, mm, mml, b_pre, x3d, part, I, S, tp, st); break;
     default: amn ? go<128, true>(mx, mx3, mm, mml, b_pre, x3d, part, I, S, tp, st) : go<128, false>(mx, mx3, mm, mml, b_pre, x3d, part, I, S, tp, st); break;
+  }
+}
+
+// Z_j for a middle mode: out[(r, b), s] = sum_q X[r, q, b] B[q, s] with X
+// [R, Q, NB] (r fastest), a batch of NB MN-major products (3xTF32, TMEM split;
+// B pre-split hi / lo).  R % 128 == 0 so no 128-row tile straddles a batch.
+bool tc_stream_batched_supported(int64_t R, int64_t Q, int64_t NB, int64_t S) {
+  return R % 128 == 0 && Q % 4 == 0 && S <= 128 && R * Q * NB < (1LL << 40) && NB < (1LL << 31) && use_ts();
+}
+void launch_stream_tc_batched(const float* X, const float* Bh, const float* Bl, float* out, int64_t R, int64_t Q,
+                              int64_t NB, int64_t S, int n_sm, cudaStream_t st) {
+  TcStreamPlan tp = plan_stream_tc(R * NB, 1, Q, S, n_sm, true);
+  tp.kb_per_split = tp.nkb;
+  tp.nsplit = 1;
+  uint64_t d4[4] = {32, (uint64_t)Q, (uint64_t)(R / 32), (uint64_t)NB};
+  uint64_t s4[3] = {(uint64_t)R * 4, 128, (uint64_t)(R * Q * 4)};
+  uint32_t b4[4] = {32, 32, 4, 1};
+  CUtensorMap mx = make_map(X, 4, d4, s4, b4, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+  uint64_t dm[2] = {(uint64_t)Q, (uint64_t)S}, sm[1] = {(uint64_t)Q * 4};
+  uint32_t bm[2] = {32, (uint32_t)tp.nt};
+  CUtensorMap mm = make_map(Bh, 2, dm, sm, bm);
+  CUtensorMap mml = make_map(Bl, 2, dm, sm, bm);
+  const int64_t I = R * NB;
+  const int rb = (int)R;
+  switch (tp.nt) {
+    case 32: go_ts<32, true>(mx, mm, mml, true, true, out, I, S, tp, st, rb); break;
+    case 64: go_ts<64, true>(mx, mm, mml, true, true, out, I, S, tp, st, rb); break;
+    case 96: go_ts<96, true>(mx, mm, mml, true, true, out, I, S, tp, st, rb); break;
+    default: go_ts<128, true>(mx, mm, mml, true, true, out, I, S, tp, st, rb); break;
   }
 }
 
