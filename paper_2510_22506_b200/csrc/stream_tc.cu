@@ -23,6 +23,7 @@
 #include <cuda_runtime.h>
 
 
+#include <algorithm>
 #include <cstdlib>
 #include <stdexcept>
 #include <string>
@@ -379,6 +380,212 @@ __global__ void __launch_bounds__(TS_THREADS, 1)
   }
 }
 
+// Persistent form of k_stream_ts for unsplit products with many row tiles
+// (the Z_j passes): one CTA per SM walks its row tiles with one continuous
+// operand pipeline; two TMEM accumulators let four epilogue warps drain tile
+// j while the MMA already accumulates tile j + 1.
+constexpr int TSP_EPI_WARPS = 4;
+constexpr int TSP_THREADS = 64 + 32 * (TS_CONV_WARPS + TSP_EPI_WARPS);
+template <int NT>
+struct TspSmem {
+  static constexpr int B_BYTES = NT * BK * 4;
+  static constexpr int STAGE_BYTES = A_BYTES + 2 * B_BYTES;
+  static constexpr int ACC = 2 * NT;  // one accumulator: [hi x (B hi | B lo)]
+  static constexpr int S_SMEM = (200 * 1024) / STAGE_BYTES > 6 ? 6 : (200 * 1024) / STAGE_BYTES;
+  static constexpr int S_TMEM = (512 - 2 * ACC) / 64;
+  static constexpr int STAGES = S_SMEM < S_TMEM ? S_SMEM : S_TMEM;
+  static constexpr int TOTAL = STAGES * STAGE_BYTES + 1024 + 256;
+};
+
+template <int NT, bool AMN>
+__global__ void __launch_bounds__(TSP_THREADS, 1)
+    k_stream_tsp(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmM,
+                 const __grid_constant__ CUtensorMap tmMl, float* __restrict__ out, int I, int S, int nkb,
+                 int n_tiles, int nPB, int b_pre, int x3d, int rows_b) {
+  using L = TspSmem<NT>;
+  constexpr int STAGES = L::STAGES;
+  static_assert(STAGES >= 2, "stage ring");
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * L::STAGE_BYTES);
+  uint64_t* conv = full + STAGES;
+  uint64_t* empty = conv + STAGES;
+  uint64_t* tfull = empty + STAGES;  // [2]
+  uint64_t* tempty = tfull + 2;      // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr int EPI0 = 2 + TS_CONV_WARPS;
+
+  if (warp == 0 && lane == 0) {
+    tc::tma_prefetch(&tmX);
+    tc::tma_prefetch(&tmM);
+    for (int s = 0; s < STAGES; ++s) {
+      tc::mbar_init(&full[s], 1);
+      tc::mbar_init(&conv[s], TS_CONV_WARPS);
+      tc::mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      tc::mbar_init(&tfull[a], 1);
+      tc::mbar_init(&tempty[a], TSP_EPI_WARPS);
+    }
+    tc::fence_barrier_init();
+  }
+  if (warp == 1) tc::tmem_alloc<512>(tmem_slot);
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0 && lane == 0) {
+    // ---------------- TMA producer
+    const uint32_t tx = A_BYTES + L::B_BYTES * (b_pre ? 2 : 1);
+    int g = 0;
+    for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+      const int i0 = t * 128;
+      for (int kb = 0; kb < nkb; ++kb, ++g) {
+        const int s = g % STAGES;
+        tc::mbar_wait(&empty[s], ((g / STAGES) & 1) ^ 1);
+        tc::mbar_expect_tx(&full[s], tx);
+        uint8_t* a = smem + s * L::STAGE_BYTES;
+        uint8_t* b = a + A_BYTES;
+        if (AMN) {
+          const int q0 = kb * BK;
+          if (rows_b) {
+            tc::tma_load_4d(a, &tmX, &full[s], 0, q0, (i0 % rows_b) / 32, i0 / rows_b);
+          } else if (x3d) {
+            tc::tma_load_3d(a, &tmX, &full[s], 0, q0, i0 / 32);
+          } else {
+#pragma unroll
+            for (int c = 0; c < 4; ++c) tc::tma_load_2d(a + c * 4096, &tmX, &full[s], i0 + 32 * c, q0);
+          }
+          tc::tma_load_2d(b, &tmM, &full[s], q0, 0);
+          if (b_pre) tc::tma_load_2d(b + L::B_BYTES, &tmMl, &full[s], q0, 0);
+        } else {
+          const int pb = (kb % nPB) * BK;
+          const int q = kb / nPB;
+          tc::tma_load_3d(a, &tmX, &full[s], pb, i0, q);
+          tc::tma_load_3d(b, &tmM, &full[s], pb, q, 0);
+          if (b_pre) tc::tma_load_3d(b + L::B_BYTES, &tmMl, &full[s], pb, q, 0);
+        }
+      }
+    }
+  } else if (warp == 1 && lane == 0) {
+    // ---------------- MMA issuer
+    constexpr uint32_t idesc2 = tc::idesc_tf32(128, 2 * NT, false, false);
+    constexpr uint32_t idesc1 = tc::idesc_tf32(128, NT, false, false);
+    int g = 0, j = 0;
+    for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++j) {
+      const int acc = j & 1;
+      tc::mbar_wait(&tempty[acc], ((j >> 1) & 1) ^ 1);
+      tc::fence_after_sync();
+      const uint32_t d = tmem + acc * L::ACC;
+      for (int kb = 0; kb < nkb; ++kb, ++g) {
+        const int s = g % STAGES;
+        tc::mbar_wait(&conv[s], (g / STAGES) & 1);
+        tc::fence_after_sync();
+        const uint32_t b = tc::smem_u32(smem + s * L::STAGE_BYTES) + A_BYTES;
+        const uint32_t ahi = tmem + 2 * L::ACC + 64 * s, alo = ahi + 32;
+#pragma unroll
+        for (int kk = 0; kk < BK / 8; ++kk) {
+          const uint64_t bd = tc::sdesc(b + kk * 32, 16, 1024);
+          tc::mma_tf32_ts(d, ahi + 8 * kk, bd, idesc2, (kb | kk) != 0);
+          tc::mma_tf32_ts(d, alo + 8 * kk, bd, idesc1, 1);
+        }
+        tc::mma_commit(&empty[s]);
+      }
+      tc::mma_commit(&tfull[acc]);
+    }
+  } else if (warp >= 2 && warp < EPI0) {
+    // ---------------- X split into TMEM (+ B split in smem when not pre-split)
+    const int q = warp & 3;
+    const int hf = (warp - 2) >> 2;
+    const int row = 32 * q + lane;
+    const int ct = threadIdx.x - 64;
+    int g = 0;
+    for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+      for (int kb = 0; kb < nkb; ++kb, ++g) {
+        const int s = g % STAGES;
+        tc::mbar_wait(&full[s], (g / STAGES) & 1);
+        const uint8_t* a = smem + s * L::STAGE_BYTES;
+        float x[16];
+        if (AMN) {
+          const float* box = reinterpret_cast<const float*>(a + (row >> 5) * 4096);
+          const int i = row & 31;
+#pragma unroll
+          for (int jj = 0; jj < 16; ++jj) {
+            const int kq = 16 * hf + jj;
+            x[jj] = box[kq * 32 + ((((i >> 3) ^ (kq & 3))) << 3) + (i & 7)];
+          }
+        } else {
+          const float4* r4 = reinterpret_cast<const float4*>(a + row * 128);
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            const float4 v = r4[(4 * hf + c) ^ (row & 7)];
+            x[4 * c] = v.x;
+            x[4 * c + 1] = v.y;
+            x[4 * c + 2] = v.z;
+            x[4 * c + 3] = v.w;
+          }
+        }
+        float lo[16];
+#pragma unroll
+        for (int jj = 0; jj < 16; ++jj) {
+          const float h = tc::tf32_rn_int(x[jj]);
+          lo[jj] = tc::tf32_rn_int(x[jj] - h);
+          x[jj] = h;
+        }
+        const uint32_t ta = tmem + ((uint32_t)(32 * q) << 16) + 2 * L::ACC + 64 * s + 16 * hf;
+        tc::tmem_st16(ta, x);
+        tc::tmem_st16(ta + 32, lo);
+        if (!b_pre) {
+          uint8_t* b = smem + s * L::STAGE_BYTES + A_BYTES;
+          tc::tf32_split_tile<true>(b, b + L::B_BYTES, L::B_BYTES / 4, ct, 32 * TS_CONV_WARPS);
+          tc::fence_proxy_async_smem();
+        }
+        tc::tmem_wait_st();
+        tc::fence_before_sync();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(&conv[s]);
+      }
+    }
+  } else if (warp >= EPI0) {
+    // ---------------- epilogue: accumulator j & 1 -> out rows, then release it
+    const int q = warp & 3;
+    const int row = 32 * q + lane;
+    int j = 0;
+    for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++j) {
+      const int acc = j & 1;
+      tc::mbar_wait(&tfull[acc], (j >> 1) & 1);
+      tc::fence_after_sync();
+      const long long i = (long long)t * 128 + row;
+      const uint32_t base = tmem + ((uint32_t)(32 * q) << 16) + acc * L::ACC;
+#pragma unroll 1
+      for (int c0 = 0; c0 < NT; c0 += 16) {
+        float v[16], w[16];
+        tc::tmem_ld16(base + c0, v);
+        tc::tmem_ld16(base + NT + c0, w);
+        if (i < I) {
+#pragma unroll
+          for (int jj = 0; jj < 16; ++jj) {
+            const int sc = c0 + jj;
+            if (sc < S) out[i + (long long)I * sc] = v[jj] + w[jj];
+          }
+        }
+      }
+      tc::fence_before_sync();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&tempty[acc]);
+    }
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  if (warp == 1) {
+    tc::fence_after_sync();
+    tc::tmem_dealloc<512>(tmem);
+  }
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   if (!fn) {
@@ -419,9 +626,33 @@ void go3(const CUtensorMap& mx, const CUtensorMap& mm, const CUtensorMap& mml, b
   if (e != cudaSuccess) throw std::runtime_error(std::string("stream_tc: ") + cudaGetErrorString(e));
 }
 
+int sm_count() {
+  static const int v = [] {
+    int d = 0, n = 148;
+    if (cudaGetDevice(&d) == cudaSuccess) cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, d);
+    return n;
+  }();
+  return v;
+}
+
 template <int NT, bool AMN>
 void go_ts(const CUtensorMap& mx, const CUtensorMap& mm, const CUtensorMap& mml, bool b_pre, bool x3d, float* part,
            int64_t I, int64_t S, const TcStreamPlan& tp, cudaStream_t st, int rows_b = 0) {
+  static const bool no_persist = getenv("FCTN_STREAM_NO_PERSIST") != nullptr;
+  if constexpr (NT <= 64) {
+    if (tp.nsplit == 1 && tp.n_mtiles > sm_count() && !no_persist && tp.nkb < (1LL << 31)) {
+      const int smem = TspSmem<NT>::TOTAL;
+      auto fn = k_stream_tsp<NT, AMN>;
+      cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      if (e != cudaSuccess) throw std::runtime_error(std::string("stream_tsp smem: ") + cudaGetErrorString(e));
+      const int grid = (int)std::min<int64_t>(tp.n_mtiles, sm_count());
+      fn<<<grid, TSP_THREADS, smem, st>>>(mx, mm, mml, part, (int)I, (int)S, (int)tp.nkb, (int)tp.n_mtiles,
+                                          (int)tp.npb, b_pre ? 1 : 0, x3d ? 1 : 0, rows_b);
+      e = cudaGetLastError();
+      if (e != cudaSuccess) throw std::runtime_error(std::string("stream_tsp: ") + cudaGetErrorString(e));
+      return;
+    }
+  }
   const int smem = TsSmem<NT>::TOTAL;
   auto fn = k_stream_ts<NT, AMN>;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);

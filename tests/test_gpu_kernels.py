@@ -17,6 +17,8 @@ def _unfold(x, k):
     ((256, 64, 8), 0, 64), ((256, 64, 8), 1, 64), ((256, 64, 8), 2, 64),
     ((48, 40, 36), 0, 81), ((48, 40, 36), 1, 27), ((48, 40, 36), 2, 9),
     ((2048, 32, 4), 0, 64), ((20, 20, 20, 20), 3, 27),
+    # > 148 row tiles, unsplit: the persistent kernel (MN-major, K-major, ragged rows / bonds)
+    ((20480, 8, 4), 0, 64), ((32, 20480, 2), 1, 64), ((16, 20608, 2), 1, 20), ((40, 19000, 2), 1, 64),
 ])
 @pytest.mark.parametrize("use_tc", [True, False])
 def test_stream_fp32_matches_numpy(dims, k, S, use_tc):
