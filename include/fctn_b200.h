@@ -156,6 +156,36 @@ int fctn_selftest_stream(int device, int dtype, int use_tc, int64_t I, int64_t P
 int fctn_selftest_chol(int device, int64_t S, int64_t H1, const double* G, const double* mu, double* Fr, double* Fi,
                        int reps, double* ms_per_launch);
 
+/* Reconstruction quality (metrics.py:33-105).  The
+ * first two modes are the image plane, every trailing-mode combination is a
+ * slice (metrics.py:19-23).  `out` (FCTN_Q_COUNT doubles): mean over slices
+ * of PSNR with the 100 dB zero-error cap (metrics.py:33-44); mean over slices
+ * of the single-window structural index (metrics.py:47-66); the squared
+ * norms behind rel_err (metrics.py:66-92) over all entries and over the mask
+ * complement, and the complement's size.  The caller forms rel_err =
+ * sqrt(ERR_SQ/REF_SQ) and applies the reference's errors (zero denominator
+ * -> ValueError; empty complement -> nan).  Status 1 for n < 2 or peak <= 0
+ * (metrics.py:20-21,35-36,50-51). */
+#define FCTN_Q_PSNR 0
+#define FCTN_Q_SSIM 1
+#define FCTN_Q_ERR_SQ 2       /* ||est - truth||^2 */
+#define FCTN_Q_REF_SQ 3       /* ||truth||^2 */
+#define FCTN_Q_OFF_ERR_SQ 4   /* ||(est - truth) off the mask||^2 */
+#define FCTN_Q_OFF_REF_SQ 5   /* ||truth off the mask||^2 */
+#define FCTN_Q_OFF_COUNT 6    /* entries off the mask */
+#define FCTN_Q_COUNT 8
+
+/* Host tensors est / truth (same shape, `dtype`), optional mask (NULL: no
+ * off-mask terms; one byte per entry, nonzero = observed).  Replaces
+ * metrics.quality_report + rel_err(mask=) (metrics.py:66-105; cli.py:207-219). */
+int fctn_quality(int device, int dtype, int n, const int64_t* dims, const void* est_F, const void* truth_F,
+                 const uint8_t* mask_F, double peak, double* out);
+
+/* The same for the context's resident X (no download): truth is a host
+ * tensor in `truth_dtype` (this rank's slab when sharded; the per-slice sums
+ * are all-reduced over ranks); mask_mode 1 uses the observation mask, 0 none. */
+int fctn_quality_ctx(fctn_ctx* ctx, const void* truth_F, int truth_dtype, int mask_mode, double peak, double* out);
+
 /* Sync the context stream. */
 int fctn_sync(fctn_ctx* ctx);
 

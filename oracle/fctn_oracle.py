@@ -519,3 +519,38 @@ def psnr(x, ref, peak=1.0) -> float:
         mse = float(np.mean((xs[:, :, t] - rs[:, :, t]) ** 2))
         vals.append(100.0 if mse == 0.0 else 10.0 * math.log10(peak * peak / mse))
     return float(np.mean(vals))
+
+
+def ssim(x, ref, peak=1.0) -> float:
+    """Slice-averaged single-window structural index (`metrics.py:47-66`):
+    plain means, population variances and covariance per slice, stabilisers
+    c1 = (0.01 peak)^2, c2 = (0.03 peak)^2."""
+    c1, c2 = (0.01 * peak) ** 2, (0.03 * peak) ** 2
+    xs = np.asarray(x, np.float64).reshape((x.shape[0], x.shape[1], -1), order="F")
+    rs = np.asarray(ref, np.float64).reshape((ref.shape[0], ref.shape[1], -1), order="F")
+    vals = []
+    for t in range(xs.shape[2]):
+        a, b = xs[:, :, t], rs[:, :, t]
+        ma, mb = float(a.mean()), float(b.mean())
+        va, vb = float(a.var()), float(b.var())
+        cov = float(((a - ma) * (b - mb)).mean())
+        vals.append((2.0 * ma * mb + c1) * (2.0 * cov + c2) / ((ma * ma + mb * mb + c1) * (va + vb + c2)))
+    return float(np.mean(vals))
+
+
+def rel_err(x, ref, mask=None) -> float:
+    """Relative Frobenius error, over the mask complement when a mask is given;
+    nan for an empty complement, ValueError for a zero denominator
+    (`metrics.py:69-92`)."""
+    x = np.asarray(x, np.float64)
+    ref = np.asarray(ref, np.float64)
+    if mask is None:
+        num, den = float(np.linalg.norm((x - ref).ravel())), float(np.linalg.norm(ref.ravel()))
+    else:
+        sel = ~np.asarray(mask, dtype=bool)
+        if not sel.any():
+            return math.nan
+        num, den = float(np.linalg.norm(x[sel] - ref[sel])), float(np.linalg.norm(ref[sel]))
+    if den == 0.0:
+        raise ValueError("zero-norm denominator in relative error")
+    return num / den

@@ -25,8 +25,9 @@ EXPORTS = [
     "fctn_create", "fctn_upload", "fctn_upload_f64", "fctn_get_x_f64", "fctn_set_factors", "fctn_set_rank", "fctn_get_factors", "fctn_get_x",
     "fctn_objective", "fctn_sweep", "fctn_plan_sweeps", "fctn_nccl_unique_id", "fctn_set_comm", "fctn_set_comm_host",
     "fctn_sync", "fctn_selftest_stream", "fctn_selftest_chol", "fctn_timer", "fctn_set_profiling", "fctn_get_profile", "fctn_last_error", "fctn_version",
-    "fctn_destroy",
+    "fctn_quality", "fctn_quality_ctx", "fctn_destroy",
 ]
+Q_PSNR, Q_SSIM, Q_ERR_SQ, Q_REF_SQ, Q_OFF_ERR_SQ, Q_OFF_REF_SQ, Q_OFF_COUNT, Q_COUNT = 0, 1, 2, 3, 4, 5, 6, 8
 K_CLASSES = ["merge", "stream_y", "gram", "reduce", "chol", "compose", "dft", "fgram", "zpass", "ysmall", "mbuild",
              "k11"]
 
@@ -102,6 +103,8 @@ def lib():
     L.fctn_timer.argtypes = [P, C.c_int, f64p]
     L.fctn_set_profiling.argtypes = [P, C.c_int]
     L.fctn_get_profile.argtypes = [P, f64p, i64p, f64p]
+    L.fctn_quality.argtypes = [C.c_int, C.c_int, C.c_int, i64p, P, P, P, C.c_double, f64p]
+    L.fctn_quality_ctx.argtypes = [P, P, C.c_int, C.c_int, C.c_double, f64p]
     L.fctn_last_error.argtypes = [P]
     L.fctn_last_error.restype = C.c_char_p
     L.fctn_version.argtypes = []
@@ -168,6 +171,24 @@ def selftest_stream(x, m, k, use_tc=True, device=0):
                                     m.ctypes.data_as(C.c_void_p), y.ctypes.data_as(C.POINTER(C.c_double)))
     check(rc)
     return y
+
+
+def quality(est: np.ndarray, truth: np.ndarray, mask=None, peak: float = 1.0, device: int = 0) -> np.ndarray:
+    """Raw quality sums (FCTN_Q_*) of two host tensors on the device."""
+    dt = F32 if (est.dtype == np.float32 and truth.dtype == np.float32) else F64
+    npd = np.float32 if dt == F32 else np.float64
+    e = np.asfortranarray(est, dtype=npd)
+    t = np.asfortranarray(truth, dtype=npd)
+    m = None
+    if mask is not None:
+        m = np.asfortranarray(mask)
+        m = m.view(np.uint8) if m.dtype == np.bool_ else np.asfortranarray(m != 0, dtype=np.uint8)
+    d, dp = _i64(e.shape)
+    out = np.zeros(Q_COUNT, dtype=np.float64)
+    check(lib().fctn_quality(int(device), dt, e.ndim, dp, e.ctypes.data_as(C.c_void_p), t.ctypes.data_as(C.c_void_p),
+                             None if m is None else m.ctypes.data_as(C.c_void_p), float(peak),
+                             out.ctypes.data_as(C.POINTER(C.c_double))))
+    return out
 
 
 def selftest_chol(G, mu, Fr, Fi, reps=1, device=0):
@@ -288,6 +309,19 @@ class Context:
 
     def sync(self):
         self._check(lib().fctn_sync(self.h))
+
+    def quality(self, truth: np.ndarray, use_mask: bool, peak: float = 1.0) -> np.ndarray:
+        """Raw quality sums (FCTN_Q_*) of the resident X against a host truth
+        tensor (this rank's slab when sharded)."""
+        if tuple(truth.shape) != self.dims:
+            raise ValueError("tensors must have identical shapes")
+        t = truth if truth.dtype in (np.float32, np.float64) else truth.astype(np.float64)
+        t = np.asfortranarray(t)
+        out = np.zeros(Q_COUNT, dtype=np.float64)
+        self._check(lib().fctn_quality_ctx(self.h, t.ctypes.data_as(C.c_void_p), F32 if t.dtype == np.float32 else F64,
+                                           int(bool(use_mask)), float(peak),
+                                           out.ctypes.data_as(C.POINTER(C.c_double))))
+        return out
 
     def set_comm_nccl(self, uid: bytes, rank: int, nranks: int):
         lo, hi = slab_of(self.dims[0], rank, nranks)

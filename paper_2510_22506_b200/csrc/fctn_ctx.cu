@@ -1702,6 +1702,118 @@ int fctn_selftest_chol(int device, int64_t S, int64_t H1, const double* G, const
   });
 }
 
+}  // extern "C"
+
+namespace fctn {
+// Both metric passes over device-resident est / truth; `reduce` sums the
+// per-slice partials over ranks (identity on one GPU).  out: FCTN_Q_COUNT.
+template <typename TE, typename TT, typename R>
+static void quality_passes(int64_t hw_local, int64_t hw_global, int64_t nslices, int n_sm, const TE* e, const TT* t,
+                           const uint8_t* mask, double peak, R&& reduce, double* out, cudaStream_t st) {
+  const QualityPlan p = quality_plan(hw_local, nslices, n_sm);
+  const double inv_hw = 1.0 / (double)hw_global;
+  double* scratch = nullptr;
+  const int64_t nd = p.part_doubles + p.sums_doubles + QUALITY_OUT;
+  CK(cudaMallocAsync((void**)&scratch, nd * sizeof(double), st));
+  double* part = scratch;
+  double* s1 = part + p.part_doubles;
+  double* s2 = s1 + nslices * QUALITY_S1;
+  double* dout = s2 + nslices * QUALITY_S2;
+  launch_quality_pass1<TE, TT>(p, e, t, mask, part, s1, st);
+  reduce(s1, nslices * QUALITY_S1);
+  launch_quality_pass2<TE, TT>(p, e, t, s1, inv_hw, part, s2, st);
+  reduce(s2, nslices * QUALITY_S2);
+  launch_quality_final(p, s1, s2, inv_hw, peak, dout, st);
+  CK(cudaGetLastError());
+  double h[QUALITY_OUT];
+  CK(cudaMemcpyAsync(h, dout, sizeof(h), cudaMemcpyDeviceToHost, st));
+  CK(cudaFreeAsync(scratch, st));
+  CK(cudaStreamSynchronize(st));
+  for (int q = 0; q < FCTN_Q_COUNT; ++q) out[q] = q < QUALITY_OUT ? h[q] : 0.0;
+}
+
+template <typename R>
+static void quality_dispatch(int te, int tt, int64_t hw_local, int64_t hw_global, int64_t nslices, int n_sm,
+                             const void* e, const void* t, const uint8_t* mask, double peak, R&& reduce, double* out,
+                             cudaStream_t st) {
+  if (te == FCTN_F64 && tt == FCTN_F64)
+    quality_passes(hw_local, hw_global, nslices, n_sm, (const double*)e, (const double*)t, mask, peak, reduce, out, st);
+  else if (te == FCTN_F32 && tt == FCTN_F32)
+    quality_passes(hw_local, hw_global, nslices, n_sm, (const float*)e, (const float*)t, mask, peak, reduce, out, st);
+  else if (te == FCTN_F32 && tt == FCTN_F64)
+    quality_passes(hw_local, hw_global, nslices, n_sm, (const float*)e, (const double*)t, mask, peak, reduce, out, st);
+  else
+    quality_passes(hw_local, hw_global, nslices, n_sm, (const double*)e, (const float*)t, mask, peak, reduce, out, st);
+}
+
+static void quality_check(int n, double peak, int dtype) {
+  if (n < 2) throw UsageError("need at least two modes");
+  if (!(peak > 0)) throw UsageError("peak must be > 0");
+  if (dtype != FCTN_F64 && dtype != FCTN_F32) throw UsageError("dtype must be FCTN_F64 or FCTN_F32");
+}
+}  // namespace fctn
+
+extern "C" {
+
+int fctn_quality(int device, int dtype, int n, const int64_t* dims, const void* est_F, const void* truth_F,
+                 const uint8_t* mask_F, double peak, double* out) {
+  return fctn::guarded(nullptr, [&] {
+    fctn::quality_check(n, peak, dtype);
+    int64_t T = 1;
+    for (int k = 0; k < n; ++k) {
+      if (dims[k] < 1) throw fctn::UsageError("extents must be >= 1");
+      T *= dims[k];
+    }
+    const int64_t hw = dims[0] * dims[1];
+    const size_t es = dtype == FCTN_F64 ? 8 : 4;
+    CK(cudaSetDevice(device));
+    int n_sm = 148;
+    CK(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, device));
+    cudaStream_t st;
+    CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    struct StreamGuard {
+      cudaStream_t s;
+      ~StreamGuard() { cudaStreamDestroy(s); }
+    } sg{st};
+    fctn::HostPin pe(est_F, T * es), pt(truth_F, T * es);
+    void *de = nullptr, *dt = nullptr;
+    uint8_t* dm = nullptr;
+    CK(cudaMallocAsync(&de, T * es, st));
+    CK(cudaMallocAsync(&dt, T * es, st));
+    if (mask_F) CK(cudaMallocAsync((void**)&dm, T, st));
+    CK(cudaMemcpyAsync(de, est_F, T * es, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(dt, truth_F, T * es, cudaMemcpyHostToDevice, st));
+    if (mask_F) CK(cudaMemcpyAsync(dm, mask_F, T, cudaMemcpyHostToDevice, st));
+    fctn::quality_dispatch(dtype, dtype, hw, hw, T / hw, n_sm, de, dt, dm, peak, [](double*, int64_t) {}, out, st);
+    CK(cudaFreeAsync(de, st));
+    CK(cudaFreeAsync(dt, st));
+    if (dm) CK(cudaFreeAsync(dm, st));
+    CK(cudaStreamSynchronize(st));
+  });
+}
+
+int fctn_quality_ctx(fctn_ctx* c, const void* truth_F, int truth_dtype, int mask_mode, double peak, double* out) {
+  return fctn::guarded(&c->impl, [&] {
+    Ctx& x = c->impl;
+    fctn::quality_check(x.gsh.n, peak, truth_dtype);
+    if (!x.uploaded) throw fctn::UsageError("no data uploaded");
+    if (mask_mode != 0 && mask_mode != 1) throw fctn::UsageError("mask_mode must be 0 or 1");
+    const int64_t T = x.sh.total();
+    const size_t es = truth_dtype == FCTN_F64 ? 8 : 4;
+    const int64_t hw_local = x.sh.dims[0] * x.sh.dims[1];
+    const int64_t hw_global = x.gsh.dims[0] * x.gsh.dims[1];
+    fctn::HostPin pt(truth_F, T * es);
+    void* dt = nullptr;
+    CK(cudaMallocAsync(&dt, T * es, x.st));
+    CK(cudaMemcpyAsync(dt, truth_F, T * es, cudaMemcpyHostToDevice, x.st));
+    fctn::quality_dispatch(x.dtype, truth_dtype, hw_local, hw_global, T / hw_local, x.n_sm, x.X[x.cur], dt,
+                           mask_mode ? x.mask : nullptr, peak,
+                           [&](double* d, int64_t nd) { x.allreduce_sum(d, nd); }, out, x.st);
+    CK(cudaFreeAsync(dt, x.st));
+    CK(cudaStreamSynchronize(x.st));
+  });
+}
+
 int fctn_sync(fctn_ctx* c) {
   return fctn::guarded(&c->impl, [&] { CK(cudaStreamSynchronize(c->impl.st)); });
 }

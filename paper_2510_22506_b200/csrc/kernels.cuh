@@ -153,4 +153,26 @@ void launch_pack_mask(const uint8_t* mask, int64_t T, uint32_t* bits, cudaStream
 // fixed-order final reduction of n x 4 partials into out[0..3]
 void launch_reduce4(const double* partials, int64_t n, double* out, cudaStream_t st);
 
+// ---------------------------------------------------------------- quality metrics (metrics.cu)
+// psnr / ssim / rel_err of metrics.py:33-105 over F-order slices of hw entries
+struct QualityPlan {
+  int64_t hw = 0, nslices = 0, seglen = 0;
+  int nseg = 0;
+  int64_t part_doubles = 0;  // segment partials scratch
+  int64_t sums_doubles = 0;  // per-slice sums (pass 1 then pass 2)
+};
+QualityPlan quality_plan(int64_t hw, int64_t nslices, int n_sm);
+static constexpr int QUALITY_S1 = 7, QUALITY_S2 = 3, QUALITY_OUT = 7;
+// per-slice [sum e, sum t, sum d^2, sum t^2, off-mask sum d^2, sum t^2, count]
+template <typename TE, typename TT>
+void launch_quality_pass1(const QualityPlan& p, const TE* est, const TT* truth, const uint8_t* mask, double* part,
+                          double* sums1, cudaStream_t st);
+// per-slice centred [sum (e-mu)^2, sum (t-mu)^2, sum (e-mu)(t-mu)]; inv_hw = 1/(global H*W)
+template <typename TE, typename TT>
+void launch_quality_pass2(const QualityPlan& p, const TE* est, const TT* truth, const double* sums1, double inv_hw,
+                          double* part, double* sums2, cudaStream_t st);
+// out[QUALITY_OUT] = [mean psnr, mean ssim, ||e-t||^2, ||t||^2, off-mask ||e-t||^2, ||t||^2, count]
+void launch_quality_final(const QualityPlan& p, const double* sums1, const double* sums2, double inv_hw, double peak,
+                          double* out, cudaStream_t st);
+
 }  // namespace fctn

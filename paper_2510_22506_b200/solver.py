@@ -145,6 +145,8 @@ class SolverResult:
     trace: list = field(default_factory=list)
     converged: bool = False
     initial_objective: float = math.nan
+    # (iteration, metrics.QualityReport) when run(..., truth=...) is given
+    quality: list = field(default_factory=list)
 
     @property
     def iterations(self) -> int:
@@ -199,6 +201,13 @@ class _Device:
             self.ctx.set_rank(f.rank.entries)
         self.ctx.set_factors(f.unfoldings(), f.versions, reset_cache)
 
+    def quality(self, truth: np.ndarray, peak: float):
+        from .metrics import QualityReport, from_sums
+        lo, hi = self.slab
+        t = truth if (lo, hi) == (0, self.dims[0]) else truth[lo:hi]
+        p, s, err, _ = from_sums(self.ctx.quality(np.asfortranarray(t), False, peak), masked=False)
+        return QualityReport(psnr=p, ssim=s, rel_err=err)
+
     def fetch_factors(self, rank: FctnRank, versions) -> FctnFactors:
         shapes = [(self.dims[k], rank.bond_product(k)) for k in range(self.n)]  # global extents
         unf = self.ctx.get_factors(shapes)
@@ -236,8 +245,14 @@ def _grow_with_continuity(dev: _Device, f: FctnFactors, cap: FctnRank, rng, scal
     return cand, extra
 
 
-def run(obs, cfg: SolverConfig, *, dtype: str = "float64", device: int | None = None, shard=None) -> SolverResult:
+def run(obs, cfg: SolverConfig, *, dtype: str = "float64", device: int | None = None, shard=None,
+        truth=None, peak: float = 1.0, quality_every: int = 0) -> SolverResult:
     """Same contract as `fctnlr.solver.run` (solver.py:277-399).
+
+    ``truth`` (the full ground-truth tensor): `metrics.quality_report(x,
+    truth, peak=peak)` (metrics.py:102-105) of the resident X is computed on
+    the device after every ``quality_every``-th sweep (0: after the last
+    one only) into ``result.quality`` — no T-sized download per report.
 
     ``shard`` (a `shard.Shard`) runs this call as one rank of a mode-0 sharded
     sweep: every rank passes the same global observation and config; the
@@ -261,6 +276,14 @@ def run(obs, cfg: SolverConfig, *, dtype: str = "float64", device: int | None = 
     if device is None:
         device = 0
 
+    if truth is not None:
+        truth = np.asarray(truth)
+        if truth.shape != dims:
+            raise ValueError("tensors must have identical shapes")
+        if peak <= 0:
+            raise ValueError("peak must be > 0")
+        if truth.dtype not in (np.float32, np.float64):
+            truth = truth.astype(np.float64)
     rng = np.random.default_rng(cfg.seed)
     f = FctnFactors.random(dims, rank, rng)
     order = tuple(range(n))
@@ -316,11 +339,16 @@ def run(obs, cfg: SolverConfig, *, dtype: str = "float64", device: int | None = 
                 mk_flops=int(ct[_native.CT_MK]), compose_flops=compose_flops, step_sq=step_sq,
                 x_norm=math.sqrt(float(stats[_native.ST_XNEW_SQ])), factor_norm=factor_norm,
                 rank_grown=grown, device_ms=float(stats[_native.ST_DEVICE_MS])))
-            if not grown and rel <= cfg.eps:
+            stop = not grown and rel <= cfg.eps
+            if truth is not None and quality_every > 0 and it % quality_every == 0 and not (stop or it == cfg.max_iters):
+                result.quality.append((it, dev.quality(truth, peak)))
+            if stop:
                 result.converged = True
                 break
             if accelerated and cfg.shuffle:
                 order = tuple(int(v) for v in rng.permutation(n))  # network.py:515-517
+        if truth is not None and result.trace:
+            result.quality.append((result.trace[-1].iteration, dev.quality(truth, peak)))
         result.x = dev.ctx.get_x_f64()
         result.slab = dev.slab
         result.factors = dev.fetch_factors(rank, versions)

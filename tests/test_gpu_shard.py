@@ -45,8 +45,9 @@ def _worker(rank, world, port, dims, dtype, out_dir):
     import paper_2510_22506_b200 as P
     values, mask = _instance(dims)
     res = P.run(P.Observation(values, mask), _cfg(len(dims)), dtype=dtype, device=0,
-                shard=P.Shard(rank, world, backend="host"))
-    np.savez(os.path.join(out_dir, f"r{rank}.npz"), x=res.x, slab=np.array(res.slab),
+                shard=P.Shard(rank, world, backend="host"), truth=values, quality_every=3)
+    q = np.array([[it, r.psnr, r.ssim, r.rel_err] for it, r in res.quality])
+    np.savez(os.path.join(out_dir, f"r{rank}.npz"), x=res.x, slab=np.array(res.slab), q=q,
              obj=np.array([r.objective for r in res.trace]), flops=np.array([r.flops for r in res.trace]),
              hits=np.array([r.cache_hits for r in res.trace]),
              *[res.factors.factor(k) for k in range(len(dims))])
@@ -60,7 +61,7 @@ def test_gpu_sharded_host_backend_matches_single(tmp_path, dims, dtype, tol):
     import paper_2510_22506_b200 as P
     mp.spawn(_worker, args=(2, _port(), dims, dtype, str(tmp_path)), nprocs=2, join=True)
     values, mask = _instance(dims)
-    ref = P.run(P.Observation(values, mask), _cfg(len(dims)), dtype=dtype)
+    ref = P.run(P.Observation(values, mask), _cfg(len(dims)), dtype=dtype, truth=values, quality_every=3)
     r = [np.load(tmp_path / f"r{i}.npz") for i in range(2)]
     x = np.concatenate([r[0]["x"], r[1]["x"]], axis=0)
     assert tuple(r[0]["slab"]) == (0, dims[0] // 2)
@@ -72,6 +73,11 @@ def test_gpu_sharded_host_backend_matches_single(tmp_path, dims, dtype, tol):
     np.testing.assert_allclose(r[0]["obj"], [t.objective for t in ref.trace], rtol=tol)
     assert list(r[0]["flops"]) == [t.flops for t in ref.trace]  # global FLOP meter
     assert list(r[0]["hits"]) == [t.cache_hits for t in ref.trace]
+    # resident-X quality: per-slice sums all-reduced over the two slabs
+    qref = np.array([[it, q.psnr, q.ssim, q.rel_err] for it, q in ref.quality])
+    assert qref[:, 0].tolist() == [3, 6]
+    for i in range(2):
+        np.testing.assert_allclose(r[i]["q"], qref, rtol=max(tol, 1e-10), atol=0)
 
 
 def test_gpu_nccl_single_rank_matches_plain():
