@@ -343,6 +343,10 @@ void launch_contract(const T* A, const T* B, T* C, const ContractDesc& d, T* scr
   const int64_t tr = (d.rows + 63) / 64, tcn = (d.cols + 63) / 64;
   const int64_t tiles = tr * tcn;
   if (tiles <= 0) return;
+  if (join_applicable(d, sizeof(T))) {
+    launch_join<T>(A, B, C, d, n_sm, st);
+    return;
+  }
   if (contract_resident<T>(A, B, C, d, n_sm, st)) return;
   int64_t ns = 1;
   if (scratch && tiles < n_sm && d.K >= 256) {

@@ -24,6 +24,10 @@ template <typename T>
 void launch_contract(const T* A, const T* B, T* C, const ContractDesc& d, T* scratch, int64_t scratch_cap, int n_sm,
                      cudaStream_t st);
 int64_t contract_split_scratch(const ContractDesc& d, int n_sm);
+// large-output contractions (join.cu): register-tiled, cp.async-staged
+bool join_applicable(const ContractDesc& d, size_t esize);
+template <typename T>
+void launch_join(const T* A, const T* B, T* C, const ContractDesc& d, int n_sm, cudaStream_t st);
 
 // generic permutation: out[o] = in[sum_d digit_d(o) * in_stride[d]]
 struct PermDesc {

@@ -87,8 +87,16 @@ LTensor Planner::contract(const LTensor& a, const LTensor& b, Executor* exec,
   if (out_labels) {
     op.out.labels = *out_labels;
   } else {
+    // Device layout of a partial: labels ascending = physical modes ascending,
+    // then bonds.  The reference's as-built order (a-free then b-free,
+    // network.py:249-258) only fixes which numbers the tensor holds, so any
+    // layout is exact; this one puts the lowest physical mode first, which is
+    // the fastest label of every M_k the partial later joins into, so the
+    // join's gathers of it are unit-stride (join.cu) whatever the visiting
+    // order.
     op.out.labels = afree;
     op.out.labels.insert(op.out.labels.end(), bfree.begin(), bfree.end());
+    std::sort(op.out.labels.begin(), op.out.labels.end());
   }
   if (out_buf >= 0) {
     op.out.buf = out_buf;

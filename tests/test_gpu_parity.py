@@ -131,3 +131,21 @@ def test_gpu_sufficient_decrease():
         assert rec.objective + 0.5 * cfg.rho * rec.step_sq <= prev + 1e-9 * abs(prev)
         prev = rec.objective
     assert case is not None
+
+
+@pytest.mark.parametrize("name", ["n4_afctnlr_shuffle", "n5_afctnlr", "n5_budget_binds", "n4_nonuniform_rank",
+                                  "n3_fctnlr", "n4_threshold_growth"])
+def test_gpu_join_kernel_on_every_contraction(name, monkeypatch):
+    """The large-output join kernel (join.cu) forced onto every contraction
+    it accepts (all tile variants, ragged tiles, scalar-store fallbacks):
+    still the reference's golden result.  The threshold is read once per
+    process, so this runs in a subprocess."""
+    import subprocess
+    import sys
+    code = (
+        "import sys; sys.path.insert(0, '.');"
+        "from tests.test_gpu_parity import test_gpu_matches_reference_golden as t;"
+        f"t({name!r}); print('ok')")
+    env = dict(__import__('os').environ, FCTN_JOIN_MIN_OUT="64")
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
