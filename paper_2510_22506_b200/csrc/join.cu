@@ -23,6 +23,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <stdexcept>
 #include <string>
@@ -374,6 +375,10 @@ void join_go(const T* A, const T* B, T* C, const ContractDesc& d, int n_sm, cuda
     p.n_fix = p.n_ct;
   }
   const size_t smem = join_smem<T, RT, CT>(d.K, p.fix);
+  if (getenv("FCTN_JOIN_TRACE"))
+    fprintf(stderr, "join rows=%lld cols=%lld K=%lld RT=%d CT=%d vec=%d vec_a=%d vec_b=%d fix=%d C=%p\n",
+            (long long)d.rows, (long long)d.cols, (long long)d.K, RT, CT, (int)p.vec, (int)p.vec_a, (int)p.vec_b, p.fix,
+            (void*)C);
   auto fn = k_join<T, RT, CT>;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) throw std::runtime_error(std::string("join smem: ") + cudaGetErrorString(e));

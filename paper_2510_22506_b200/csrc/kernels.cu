@@ -7,6 +7,7 @@
 #include <cstdio>
 #include <stdexcept>
 #include <string>
+#include <type_traits>
 
 #include "kernels.cuh"
 
@@ -252,7 +253,8 @@ __global__ void __launch_bounds__(256) k_contract_rescol(const T* __restrict__ A
   extern __shared__ __align__(16) unsigned char smraw[];
   const int K = (int)d.K, cols = (int)d.cols;
   T* Bs = reinterpret_cast<T*>(smraw);                            // [K][cols]
-  int64_t* sCC = reinterpret_cast<int64_t*>(Bs + (size_t)K * cols);  // [cols]
+  // the int64 tables start 8-byte aligned whatever K * cols is
+  int64_t* sCC = reinterpret_cast<int64_t*>(smraw + (((size_t)K * cols * sizeof(T) + 7) & ~(size_t)7));  // [cols]
   int64_t* sKA = sCC + cols;                                      // [K]
   for (int e = threadIdx.x; e < K * cols; e += blockDim.x) {
     const int k = e / cols, c = e % cols;
@@ -299,7 +301,7 @@ __global__ void __launch_bounds__(256) k_contract_rescol(const T* __restrict__ A
 template <typename T, int KMAX>
 static bool rescol_go(const T* A, const T* B, T* C, const ContractDesc& d, int n_sm, cudaStream_t st) {
   constexpr int CB = 8;
-  const size_t smem = (size_t)d.K * d.cols * sizeof(T) + (d.cols + d.K) * sizeof(int64_t);
+  const size_t smem = (((size_t)d.K * d.cols * sizeof(T) + 7) & ~(size_t)7) + (d.cols + d.K) * sizeof(int64_t);
   if (smem > 160 * 1024) return false;
   auto fn = k_contract_rescol<T, KMAX, CB>;
   if (smem > 48 * 1024) {
@@ -343,6 +345,12 @@ void launch_contract(const T* A, const T* B, T* C, const ContractDesc& d, T* scr
   const int64_t tr = (d.rows + 63) / 64, tcn = (d.cols + 63) / 64;
   const int64_t tiles = tr * tcn;
   if (tiles <= 0) return;
+  if constexpr (std::is_same<T, float>::value) {
+    if (tc_join_applicable(d)) {
+      launch_join_tc(A, B, C, d, n_sm, st);
+      return;
+    }
+  }
   if (join_applicable(d, sizeof(T))) {
     launch_join<T>(A, B, C, d, n_sm, st);
     return;

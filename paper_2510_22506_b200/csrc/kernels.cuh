@@ -28,6 +28,9 @@ int64_t contract_split_scratch(const ContractDesc& d, int n_sm);
 bool join_applicable(const ContractDesc& d, size_t esize);
 template <typename T>
 void launch_join(const T* A, const T* B, T* C, const ContractDesc& d, int n_sm, cudaStream_t st);
+// fp32 large-output contractions on the tensor cores (join_tc.cu, 3xTF32)
+bool tc_join_applicable(const ContractDesc& d);
+void launch_join_tc(const float* A, const float* B, float* C, const ContractDesc& d, int n_sm, cudaStream_t st);
 
 // generic permutation: out[o] = in[sum_d digit_d(o) * in_stride[d]]
 struct PermDesc {
