@@ -93,7 +93,11 @@ __device__ __forceinline__ void tmem_ld16_async(uint32_t taddr, uint32_t* r) {
 }
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
-template <int NCOL>
+// PMN: the P tile is MN-major (SWIZZLE_128B with 32-byte atoms, the layout a
+// TMA SWIZZLE_128B_ATOM_32B box writes: 32-row boxes of 4 KB, K row kq holds
+// 32 consecutive rows, 8-float atoms XOR (kq & 3)) so 4 consecutive rows of
+// one K index are one 16-byte cp.async; else K-major SW128 with 4-byte gathers.
+template <int NCOL, bool PMN>
 __global__ void __launch_bounds__(NTHR, 1)
     k_join_tc(const float* __restrict__ Pg, const float* __restrict__ Qg, float* __restrict__ C, const TcJoinArgs a) {
   extern __shared__ uint8_t smem_raw[];
@@ -181,6 +185,7 @@ __global__ void __launch_bounds__(NTHR, 1)
     int issued = 0;
     int64_t iss_op = -1;  // row offset of the tile being issued
     int64_t iss_t = -1;
+    int64_t p_m0 = 0;
     auto issue = [&](int i) {  // gathers of stage i (tile t0 + i / nkb, K block i % nkb)
       const int s = i % S;
       tc::mbar_wait(&pempty[s], ((i / S) & 1) ^ 1);
@@ -190,21 +195,49 @@ __global__ void __launch_bounds__(NTHR, 1)
         iss_t = t;
         int64_t mt, nt;
         tile_mn(t, mt, nt);
-        const int64_t m = mt * 128 + lt;
+        p_m0 = mt * 128;
+        const int64_t m = PMN ? p_m0 + 4 * (lt & 31) : p_m0 + lt;
         int64_t oc;
         iss_op = -1;
         if (m < Pn) md2((uint32_t)m, PS, iss_op, oc);
       }
       uint8_t* hi = pst + (size_t)s * 2 * P_TILE;
+      if (PMN) {
+        const int mn4 = lt & 31, kq0 = lt >> 5;
+        const int i = (4 * mn4) & 31;
+        uint8_t* box = hi + (mn4 >> 3) * 4096;
+        const int64_t m0 = p_m0 + 4 * mn4;
+        const bool full4 = m0 + 3 < Pn;
 #pragma unroll
-      for (int k = 0; k < 32; ++k) {
-        const int64_t ko = koffP[kb * 32 + k];
-        const bool ok = iss_op >= 0 && ko >= 0;
-        const uint32_t dst = tc::smem_u32(hi + swz(lt, k >> 2) + (k & 3) * 4);
-        // no memory clobber: the offset loads may be scheduled ahead; the
-        // wait_group below orders the smem reads
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(dst),
-                     "l"(Pg + (ok ? iss_op + ko : 0)), "r"(ok ? 4 : 0));
+        for (int j = 0; j < 8; ++j) {
+          const int k = kq0 + 4 * j;
+          const int64_t ko = koffP[kb * 32 + k];
+          const uint32_t dst = tc::smem_u32(box + (k * 32 + (((i >> 3) ^ (k & 3)) << 3) + (i & 7)) * 4);
+          if (full4 || m0 >= Pn) {
+            const bool ok = full4 && ko >= 0;
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst),
+                         "l"(Pg + (ok ? iss_op + ko : 0)), "r"(ok ? 16 : 0));
+          } else {  // ragged end of P: rows one by one
+            for (int e = 0; e < 4; ++e) {
+              int64_t o1 = -1, oc;
+              if (m0 + e < Pn) md2((uint32_t)(m0 + e), PS, o1, oc);
+              const bool ok = o1 >= 0 && ko >= 0;
+              asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(dst + 4 * e),
+                           "l"(Pg + (ok ? o1 + ko : 0)), "r"(ok ? 4 : 0));
+            }
+          }
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < 32; ++k) {
+          const int64_t ko = koffP[kb * 32 + k];
+          const bool ok = iss_op >= 0 && ko >= 0;
+          const uint32_t dst = tc::smem_u32(hi + swz(lt, k >> 2) + (k & 3) * 4);
+          // no memory clobber: the offset loads may be scheduled ahead; the
+          // wait_group below orders the smem reads
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(dst),
+                       "l"(Pg + (ok ? iss_op + ko : 0)), "r"(ok ? 4 : 0));
+        }
       }
       asm volatile("cp.async.commit_group;" ::: "memory");
     };
@@ -257,6 +290,21 @@ __global__ void __launch_bounds__(NTHR, 1)
       const int s = i % S;
       uint8_t* hi = pst + (size_t)s * 2 * P_TILE;
       uint8_t* lo = hi + P_TILE;
+      if (PMN) {  // the 8 chunks this thread gathered
+        const int mn4 = lt & 31, kq0 = lt >> 5, ii = (4 * mn4) & 31;
+        const uint32_t bo = (mn4 >> 3) * 4096;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int k = kq0 + 4 * j;
+          const uint32_t off = bo + (k * 32 + (((ii >> 3) ^ (k & 3)) << 3) + (ii & 7)) * 4;
+          const float4 v = *reinterpret_cast<const float4*>(hi + off);
+          const float x[4] = {v.x, v.y, v.z, v.w};
+          float4 h, l;
+          split4(x, h, l);
+          sts128(hi + off, h);
+          sts128(lo + off, l);
+        }
+      } else {
 #pragma unroll
       for (int c4 = 0; c4 < 8; ++c4) {
         const float4 v = *reinterpret_cast<const float4*>(hi + swz(lt, c4));
@@ -266,6 +314,7 @@ __global__ void __launch_bounds__(NTHR, 1)
         sts128(hi + swz(lt, c4), h);
         sts128(lo + swz(lt, c4), l);
       }
+      }
       tc::fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(&pfull[s]);
@@ -273,7 +322,7 @@ __global__ void __launch_bounds__(NTHR, 1)
   } else if (warp == 8) {
     // ------------------------------------------------ MMA issuer
     if (lane == 0) {
-      const uint32_t idesc = tc::idesc_tf32(128, NT, false, false);
+      const uint32_t idesc = tc::idesc_tf32(128, NT, PMN, false);
       int64_t cur_nt = -1;
       int qphase = 0;
       int it = 0;
@@ -298,7 +347,8 @@ __global__ void __launch_bounds__(NTHR, 1)
           const uint32_t qh = tc::smem_u32(qt + (size_t)kb * 2 * q_block), ql = qh + (uint32_t)q_block;
 #pragma unroll
           for (int kk = 0; kk < JK / 8; ++kk) {
-            const uint64_t ad = tc::sdesc(ph + kk * 32, 16, 1024), adl = tc::sdesc(pl + kk * 32, 16, 1024);
+            const uint64_t ad = PMN ? tc::sdesc(ph + kk * 1024, 4096, 512, 1) : tc::sdesc(ph + kk * 32, 16, 1024);
+            const uint64_t adl = PMN ? tc::sdesc(pl + kk * 1024, 4096, 512, 1) : tc::sdesc(pl + kk * 32, 16, 1024);
             const uint64_t bd = tc::sdesc(qh + kk * 32, 16, 1024), bdl = tc::sdesc(ql + kk * 32, 16, 1024);
             tc::mma_tf32(acc, adl, bd, idesc, (kb | kk) != 0);
             tc::mma_tf32(acc, ad, bdl, idesc, 1);
@@ -438,10 +488,22 @@ void launch_join_tc(const float* A, const float* B, float* C, const ContractDesc
   }
   a.vec_n = vec_n;
   const float* P = a.p_is_rows ? A : B;
+  // P rows: 4 consecutive indices = 4 consecutive, 16-byte aligned operand entries
+  bool vec_p = reinterpret_cast<uintptr_t>(P) % 16 == 0 && !getenv("FCTN_TC_JOIN_KMAJOR");
+  {
+    const int n = a.p_is_rows ? d.nr : d.nc;
+    const int64_t* ext = a.p_is_rows ? d.r_ext : d.c_ext;
+    const int64_t* so = a.p_is_rows ? d.r_sa : d.c_sb;
+    const int64_t* ko = a.p_is_rows ? d.k_sa : d.k_sb;
+    vec_p = vec_p && n >= 1 && so[0] == 1 && ext[0] % 4 == 0;
+    for (int q = 1; q < n && vec_p; ++q) vec_p = so[q] % 4 == 0;
+    for (int q = 0; q < d.nk && vec_p; ++q) vec_p = ko[q] % 4 == 0;
+  }
   const float* Q = a.p_is_rows ? B : A;
   if (getenv("FCTN_JOIN_TRACE")) {
-    fprintf(stderr, "join_tc rows=%lld cols=%lld K=%lld p_rows=%d vec_n=%d ntile=%d nkb=%d |", (long long)d.rows,
-            (long long)d.cols, (long long)d.K, (int)a.p_is_rows, (int)a.vec_n, a.ntile, a.nkb);
+    fprintf(stderr, "join_tc rows=%lld cols=%lld K=%lld p_rows=%d vec_n=%d vec_p=%d ntile=%d nkb=%d |",
+            (long long)d.rows, (long long)d.cols, (long long)d.K, (int)a.p_is_rows, (int)a.vec_n, (int)vec_p,
+            a.ntile, a.nkb);
     for (int q = 0; q < d.nr; ++q) fprintf(stderr, " r(%lld,%lld,%lld)", (long long)d.r_ext[q], (long long)d.r_sa[q], (long long)d.r_sc[q]);
     for (int q = 0; q < d.nc; ++q) fprintf(stderr, " c(%lld,%lld,%lld)", (long long)d.c_ext[q], (long long)d.c_sb[q], (long long)d.c_sc[q]);
     fprintf(stderr, " C=%p\n", (void*)C);
@@ -453,9 +515,15 @@ void launch_join_tc(const float* A, const float* B, float* C, const ContractDesc
     e = cudaGetLastError();
     if (e != cudaSuccess) throw std::runtime_error(std::string("join_tc: ") + cudaGetErrorString(e));
   };
-  if (a.ntile <= 64) go(k_join_tc<64>);
-  else if (a.ntile <= 128) go(k_join_tc<128>);
-  else go(k_join_tc<256>);
+  if (vec_p) {
+    if (a.ntile <= 64) go(k_join_tc<64, true>);
+    else if (a.ntile <= 128) go(k_join_tc<128, true>);
+    else go(k_join_tc<256, true>);
+  } else {
+    if (a.ntile <= 64) go(k_join_tc<64, false>);
+    else if (a.ntile <= 128) go(k_join_tc<128, false>);
+    else go(k_join_tc<256, false>);
+  }
 }
 
 }  // namespace fctn

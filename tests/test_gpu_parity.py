@@ -151,8 +151,10 @@ def test_gpu_join_kernel_on_every_contraction(name, monkeypatch):
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
 
 
-@pytest.mark.parametrize("name,dims", [("c5", (12, 10, 9, 8, 7)), ("c3", (20, 18, 3, 9)), ("c5", (17, 13, 6, 5, 11))])
-def test_gpu_fp32_tc_join_on_every_contraction(name, dims):
+@pytest.mark.parametrize("name,dims,kmajor", [("c5", (12, 10, 9, 8, 7), False), ("c3", (20, 18, 3, 9), False),
+                                               ("c5", (17, 13, 6, 5, 11), False), ("c5", (12, 8, 8, 4, 12), False),
+                                               ("c5", (12, 8, 8, 4, 12), True)])
+def test_gpu_fp32_tc_join_on_every_contraction(name, dims, kmajor):
     """FP32 with the tensor-core join (join_tc.cu) forced onto every
     contraction it accepts (ragged 128-row tiles, odd N tiles, both operand
     orientations, scalar and vector epilogues): the FP32 bound against the
@@ -165,5 +167,7 @@ def test_gpu_fp32_tc_join_on_every_contraction(name, dims):
         "from tests.test_gpu_parity import test_gpu_fp32_variant_scaled as t;"
         f"t({name!r}, {dims!r}, 6); print('ok')")
     env = dict(os.environ, FCTN_JOIN_MIN_OUT="64")
+    if kmajor:  # the K-major P tile path (4-byte gathers) instead of MN-major 16-byte gathers
+        env["FCTN_TC_JOIN_KMAJOR"] = "1"
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
