@@ -10,15 +10,16 @@
 // of the output it writes; the MMA makes the operand reuse free and leaves the
 // M_k store as the only real cost.
 //
-// Warp roles (288 threads):
-//   warps 0-3  epilogue: tcgen05.ld 32 lanes x 16 columns, global stores —
+// Warp roles (416 threads):
+//   warps 0-7  epilogue (two per TMEM lane quadrant, alternate 16-column
+//              chunks): tcgen05.ld 32 lanes x 16 columns, global stores —
 //              coalesced across lanes when P holds the output's fastest label,
 //              128-bit per thread along n when Q does (vec_n)
-//   warps 4-7  loaders: gather P rows (lane = row; unit stride by the
+//   warps 8-11 loaders: gather P rows (lane = row; unit stride by the
 //              physical-modes-first partial layout, plan.cpp) and the Q tile,
 //              round/split to TF32 hi/lo, write the SWIZZLE_128B K-major
 //              layout UMMA reads; one 32-wide K block of a P tile per stage
-//   warp 8     TMEM allocation + single-thread MMA issue
+//   warp 12    TMEM allocation + single-thread MMA issue
 // Tiles: CTA b owns a contiguous range of (nt-major, mt-minor) tiles so the
 // resident Q tile changes rarely; two TMEM accumulators overlap the epilogue
 // of tile j with the MMAs of tile j+1.
@@ -40,7 +41,8 @@ namespace {
 
 constexpr int JK = 32;           // fp32 per K block (one 128-byte row)
 constexpr int P_TILE = 128 * JK * 4;  // 16 KB (hi or lo)
-constexpr int NTHR = 288;
+constexpr int NTHR = 416;  // 8 epilogue + 4 loader + 1 MMA warps
+constexpr int EPI = 256;   // epilogue threads
 
 struct TcJoinArgs {
   ContractDesc d;   // rows/cols as in kernels.cuh
@@ -154,11 +156,11 @@ __global__ void __launch_bounds__(NTHR, 1)
     tc::mbar_init(qempty, 1);
     for (int b = 0; b < 2; ++b) {
       tc::mbar_init(&tfull[b], 1);
-      tc::mbar_init(&tempty[b], 4);
+      tc::mbar_init(&tempty[b], EPI / 32);
     }
     tc::fence_barrier_init();
   }
-  if (warp == 8) tc::tmem_alloc<2 * NCOL>(tmem_slot);
+  if (warp == 12) tc::tmem_alloc<2 * NCOL>(tmem_slot);
   tc::fence_before_sync();
   __syncthreads();
   tc::fence_after_sync();
@@ -172,12 +174,12 @@ __global__ void __launch_bounds__(NTHR, 1)
     mt = t - nt * a.n_mt;
   };
 
-  if (warp >= 4 && warp < 8) {
+  if (warp >= 8 && warp < 12) {
     // ------------------------------------------------ loaders
     // P stages: cp.async gathers of this thread's row straight into the
     // swizzled hi tile, up to PD stages in flight; when a stage has landed it
     // is split in place (hi) and into the lo tile, then published.
-    const int lt = threadIdx.x - 128;  // 0..127 = row of the P tile
+    const int lt = threadIdx.x - EPI;  // 0..127 = row of the P tile
     const int PD = S - 1 < 4 ? S - 1 : 4;
     const int n_st = (int)(t1 - t0) * nkb;  // stages this CTA consumes
     int64_t cur_nt = -1;
@@ -319,7 +321,7 @@ __global__ void __launch_bounds__(NTHR, 1)
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(&pfull[s]);
     }
-  } else if (warp == 8) {
+  } else if (warp == 12) {
     // ------------------------------------------------ MMA issuer
     if (lane == 0) {
       const uint32_t idesc = tc::idesc_tf32(128, NT, PMN, false);
@@ -363,23 +365,26 @@ __global__ void __launch_bounds__(NTHR, 1)
       }
     }
   } else {
-    // ------------------------------------------------ epilogue (warps 0-3 = TMEM lane quadrants)
-    const int q = warp;  // lanes 32q .. 32q+31
+    // ------------------------------------------------ epilogue: warps w and w + 4 share TMEM lane
+    // quadrant w & 3 and take alternate 16-column chunks
+    const int q = warp & 3, half = warp >> 2;  // lanes 32q .. 32q+31
     int64_t cur_nt = -1;
+    bool nfull = false;  // every column of the N tile exists
     int j = 0;
     for (int64_t t = t0; t < t1; ++t, ++j) {
       int64_t mt, nt;
       tile_mn(t, mt, nt);
       if (nt != cur_nt) {
-        tc::named_bar(1, 128);  // previous tile's readers of offN are done
-        for (int r = threadIdx.x; r < NT; r += 128) {
+        tc::named_bar(1, EPI);  // previous tile's readers of offN are done
+        for (int r = threadIdx.x; r < NT; r += EPI) {
           const int64_t n = nt * NT + r;
           int64_t oq, o = -1;
           if (n < Qn) md2((uint32_t)n, QS, oq, o);
           offN[r] = (int32_t)o;  // M_k < 2^31 entries (tc_join_applicable)
         }
-        tc::named_bar(1, 128);
+        tc::named_bar(1, EPI);
         cur_nt = nt;
+        nfull = (nt + 1) * NT <= Qn;
       }
       const int64_t m = mt * 128 + q * 32 + lane;
       int64_t op, om = -1;
@@ -394,10 +399,14 @@ __global__ void __launch_bounds__(NTHR, 1)
       const uint32_t offN_s = tc::smem_u32(offN);
       float* Cm = C + (om >= 0 ? om : 0);
       uint32_t r0[16], r1[16];
-      tmem_ld16_async(acc, r0);
-      tmem_wait_ld();
-      for (int n0 = 0; n0 < NT; n0 += 16) {
-        if (n0 + 16 < NT) tmem_ld16_async(acc + n0 + 16, r1);
+      const int nch = NT / 16;
+      if (half < nch) {
+        tmem_ld16_async(acc + 16 * half, r0);
+        tmem_wait_ld();
+      }
+      for (int c = half; c < nch; c += 2) {
+        const int n0 = 16 * c;
+        if (c + 2 < nch) tmem_ld16_async(acc + n0 + 32, r1);
         int o[16];
 #pragma unroll
         for (int j4 = 0; j4 < 4; ++j4)
@@ -408,7 +417,7 @@ __global__ void __launch_bounds__(NTHR, 1)
           if (a.vec_n) {
 #pragma unroll
             for (int j4 = 0; j4 < 4; ++j4) {
-              if (o[4 * j4 + 3] >= 0) {
+              if (nfull || o[4 * j4 + 3] >= 0) {
                 *reinterpret_cast<float4*>(Cm + o[4 * j4]) =
                     make_float4(__uint_as_float(r0[4 * j4]), __uint_as_float(r0[4 * j4 + 1]),
                                 __uint_as_float(r0[4 * j4 + 2]), __uint_as_float(r0[4 * j4 + 3]));
@@ -418,6 +427,9 @@ __global__ void __launch_bounds__(NTHR, 1)
                   if (o[4 * j4 + e] >= 0) Cm[o[4 * j4 + e]] = __uint_as_float(r0[4 * j4 + e]);
               }
             }
+          } else if (nfull) {
+#pragma unroll
+            for (int e = 0; e < 16; ++e) Cm[o[e]] = __uint_as_float(r0[e]);
           } else {
 #pragma unroll
             for (int e = 0; e < 16; ++e)
@@ -434,7 +446,7 @@ __global__ void __launch_bounds__(NTHR, 1)
     }
   }
   __syncthreads();
-  if (warp == 8) tc::tmem_dealloc<2 * NCOL>(tmem);
+  if (warp == 12) tc::tmem_dealloc<2 * NCOL>(tmem);
 }
 
 size_t tcj_smem(int nkb, int ntile, int pstages) {
