@@ -276,11 +276,15 @@ def run_ours(args, wl, name):
     per_launch_ms = d["ms"] / max(d["launches"], 1)
     per_launch_bytes = d["bytes"] / max(d["launches"], 1)
     achieved = per_launch_bytes / (per_launch_ms / 1e3) / 1e9
-    traffic = load_traffic(name).get(dname)
+    tr = load_traffic(name).get(dname)
+    traffic = tr["traffic"] if isinstance(tr, dict) else tr
     roofline = {"bound": "hbm", "kernel": dname, "achieved": round(achieved, 1), "peak": pk["hbm_gbs"],
                 "unit": "GB/s", "frac": round(achieved / pk["hbm_gbs"], 4), "traffic": traffic,
                 "peak_source": pk["source"], "share_of_step": round(d["ms"] / prof_ms, 4),
                 "launch_ms": round(per_launch_ms, 4), "algorithmic_bytes_per_launch": per_launch_bytes}
+    if isinstance(tr, dict):
+        roofline["traffic_note"] = (f"DRAM bytes of one captured launch ({tr.get('kernel')}, algorithmic "
+                                    f"{tr.get('algorithmic')} B) — {tr.get('capture')}")
     bst, bmin = sweep_bytes(wl.dims, wl.rank, b, lasts)
     sweep_roof = {"B_stream_GB": round(bst / 1e9, 4), "B_min_GB": round(bmin / 1e9, 4),
                   "achieved_GBs": round(bst / (ms_step / 1e3) / 1e9, 1),
