@@ -153,7 +153,7 @@ def test_gpu_join_kernel_on_every_contraction(name, monkeypatch):
 
 @pytest.mark.parametrize("name,dims,kmajor", [("c5", (12, 10, 9, 8, 7), False), ("c3", (20, 18, 3, 9), False),
                                                ("c5", (17, 13, 6, 5, 11), False), ("c5", (12, 8, 8, 4, 12), False),
-                                               ("c5", (12, 8, 8, 4, 12), True)])
+                                               ("c5", (12, 8, 8, 4, 12), True), ("c5", (32, 16, 8, 4, 32), False)])
 def test_gpu_fp32_tc_join_on_every_contraction(name, dims, kmajor):
     """FP32 with the tensor-core join (join_tc.cu) forced onto every
     contraction it accepts (ragged 128-row tiles, odd N tiles, both operand
