@@ -164,19 +164,40 @@ __device__ __forceinline__ float tf32_rn(float x) {
 __device__ __forceinline__ float tf32_rn_int(float x) {
   return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
 }
+__device__ __forceinline__ float4 lds128(uint32_t a) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sts128(uint32_t a, float4 v) {
+  asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(a), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w));
+}
+// Explicit shared-memory accesses, four 16-B loads issued before any store:
+// through generic pointers the compiler had to order each load after the
+// previous iteration's stores (ncu: the split loop serialised on load latency
+// in the c5 stream and compose converters).
 template <bool SPLIT>
 __device__ __forceinline__ void tf32_split_tile(uint8_t* hi, uint8_t* lo, int nfloat, int tid, int nthr) {
-  float4* h4 = reinterpret_cast<float4*>(hi);
-  float4* l4 = reinterpret_cast<float4*>(lo);
-  for (int e = tid; e < nfloat / 4; e += nthr) {
-    const float4 v = h4[e];
-    float4 h;
-    h.x = tf32_rn(v.x);
-    h.y = tf32_rn(v.y);
-    h.z = tf32_rn(v.z);
-    h.w = tf32_rn(v.w);
-    h4[e] = h;
-    if (SPLIT) l4[e] = make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w);
+  const uint32_t hs = smem_u32(hi), ls = smem_u32(lo);
+  const int n4 = nfloat / 4;
+  int e = tid;
+  for (; e + 3 * nthr < n4; e += 4 * nthr) {
+    float4 v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) v[u] = lds128(hs + 16u * (uint32_t)(e + u * nthr));
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const float4 h = make_float4(tf32_rn_int(v[u].x), tf32_rn_int(v[u].y), tf32_rn_int(v[u].z), tf32_rn_int(v[u].w));
+      sts128(hs + 16u * (uint32_t)(e + u * nthr), h);
+      if (SPLIT)
+        sts128(ls + 16u * (uint32_t)(e + u * nthr), make_float4(v[u].x - h.x, v[u].y - h.y, v[u].z - h.z, v[u].w - h.w));
+    }
+  }
+  for (; e < n4; e += nthr) {
+    const float4 v = lds128(hs + 16u * (uint32_t)e);
+    const float4 h = make_float4(tf32_rn_int(v.x), tf32_rn_int(v.y), tf32_rn_int(v.z), tf32_rn_int(v.w));
+    sts128(hs + 16u * (uint32_t)e, h);
+    if (SPLIT) sts128(ls + 16u * (uint32_t)e, make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w));
   }
 }
 
