@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstdio>
 #include <stdexcept>
 #include <string>
@@ -339,12 +340,50 @@ int64_t contract_split_scratch(const ContractDesc& d, int n_sm) {
   return ns * d.rows * d.cols;
 }
 
+// Small outputs (a handful of 64 x 64 tiles, e.g. the fp64 Gram network's
+// s_k x s_k result at c4: one tile, one CTA, ~25 us of serial K loop): one
+// warp per output column block, lanes along rows, K split over the 8 warps
+// of a CTA and reduced in shared memory in a fixed order.
+template <typename T>
+__global__ void __launch_bounds__(256) k_contract_small(const T* __restrict__ A, const T* __restrict__ B,
+                                                        T* __restrict__ C, const ContractDesc d) {
+  __shared__ T red[8][32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t r = (int64_t)blockIdx.x * 32 + lane;  // output row (lanes: C's fastest label)
+  const int64_t c = blockIdx.y;                       // output column
+  int64_t oa = 0, orc = 0, ob = 0, oc = 0;
+  const bool ok = r < d.rows;
+  if (ok) md_offsets(r, d.nr, d.r_ext, d.r_sa, d.r_sc, oa, orc);
+  md_offsets(c, d.nc, d.c_ext, d.c_sb, d.c_sc, ob, oc);
+  T acc = T(0);
+  if (ok)
+    for (int64_t k = warp; k < d.K; k += 8) {
+      int64_t ka, kb;
+      md_offsets(k, d.nk, d.k_ext, d.k_sa, d.k_sb, ka, kb);
+      acc += A[oa + ka] * B[ob + kb];
+    }
+  red[warp][lane] = acc;
+  __syncthreads();
+  if (warp == 0 && ok) {
+    T v = red[0][lane];
+#pragma unroll
+    for (int w = 1; w < 8; ++w) v += red[w][lane];
+    C[orc + oc] = v;
+  }
+}
+
 template <typename T>
 void launch_contract(const T* A, const T* B, T* C, const ContractDesc& d, T* scratch, int64_t scratch_cap, int n_sm,
                      cudaStream_t st) {
   const int64_t tr = (d.rows + 63) / 64, tcn = (d.cols + 63) / 64;
   const int64_t tiles = tr * tcn;
   if (tiles <= 0) return;
+  if (tiles <= 4 && d.K <= 4096 && d.cols <= 65535 && d.rows * d.cols >= 256 && !getenv("FCTN_NO_SMALL_CONTRACT")) {
+    dim3 grid((unsigned)((d.rows + 31) / 32), (unsigned)d.cols);
+    k_contract_small<T><<<grid, 256, 0, st>>>(A, B, C, d);
+    check_launch("contract_small");
+    return;
+  }
   if constexpr (std::is_same<T, float>::value) {
     if (tc_join_applicable(d)) {
       launch_join_tc(A, B, C, d, n_sm, st);
