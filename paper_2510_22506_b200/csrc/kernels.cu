@@ -517,7 +517,7 @@ void launch_axpy(double* y, const double* x, double a, int64_t n, cudaStream_t s
 //     A values are warp-uniform.
 // fp64 accumulation, deterministic.
 template <typename T, int RC, int RA, int G>
-__global__ void __launch_bounds__(256) k_yzl(const T* __restrict__ Z, const T* __restrict__ A, YzArgs p,
+__global__ void __launch_bounds__(256, 2) k_yzl(const T* __restrict__ Z, const T* __restrict__ A, YzArgs p,
                                              double* __restrict__ Y, int64_t r_chunk) {
   const int64_t bz = blockIdx.x % p.Rz, o0 = (blockIdx.x / p.Rz) * G;
   const int64_t rows = p.Ir * p.Io;
@@ -529,22 +529,31 @@ __global__ void __launch_bounds__(256) k_yzl(const T* __restrict__ Z, const T* _
 #pragma unroll
     for (int c = 0; c < RA; ++c) acc[g][c] = 0.0;
   for (int64_t r = r_lo + threadIdx.x; r < r_hi; r += 256) {
-    T a[RC][RA];
+    // the RC-term inner products in the data precision (fp32 for the FP32
+    // variant: FFMA at 2x the fp64 rate), accumulated over rows in fp64; one
+    // bond of A at a time keeps the register tile small
+    T in[G][RA];
 #pragma unroll
-    for (int b = 0; b < RC; ++b)
+    for (int g = 0; g < G; ++g)
 #pragma unroll
-      for (int c = 0; c < RA; ++c) a[b][c] = A[r + p.Ir * (b * p.ac + c * p.aa)];
+      for (int c = 0; c < RA; ++c) in[g][c] = T(0);
 #pragma unroll
-    for (int g = 0; g < G; ++g) {
-      const int64_t o = o0 + g;
-      if (o >= p.Io) break;
+    for (int b = 0; b < RC; ++b) {
+      T ab[RA];
 #pragma unroll
-      for (int b = 0; b < RC; ++b) {
-        const double z = (double)Z[r + p.Ir * o + rows * (b * p.zc + bz * p.zk)];
+      for (int c = 0; c < RA; ++c) ab[c] = A[r + p.Ir * (b * p.ac + c * p.aa)];
 #pragma unroll
-        for (int c = 0; c < RA; ++c) acc[g][c] += z * (double)a[b][c];
+      for (int g = 0; g < G; ++g) {
+        const int64_t o = o0 + g < p.Io ? o0 + g : p.Io - 1;  // clamped; rows past Io are never stored
+        const T z = Z[r + p.Ir * o + rows * (b * p.zc + bz * p.zk)];
+#pragma unroll
+        for (int c = 0; c < RA; ++c) in[g][c] = fma(z, ab[c], in[g][c]);
       }
     }
+#pragma unroll
+    for (int g = 0; g < G; ++g)
+#pragma unroll
+      for (int c = 0; c < RA; ++c) acc[g][c] += (double)in[g][c];
   }
   __shared__ double red[8][G * RA];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -607,11 +616,13 @@ __global__ void __launch_bounds__(256) k_yzs(const T* __restrict__ Z, const T* _
 
 template <typename T, int R>
 static int yzl_go(const T* Z, const T* Al, const YzArgs& a, double* Y, double* part, cudaStream_t st) {
-  constexpr int G = 8;
+  constexpr int G = R * R > 32 ? 4 : 8;  // G x R fp64 accumulators + R x R operands stay in registers
   const int64_t nxy = a.Rz * ((a.Io + G - 1) / G);
-  // split the contracted rows so that the grid covers the GPU; partials reduced in order
-  int64_t rs = (4 * 148 + nxy - 1) / nxy;
-  rs = std::max<int64_t>(1, std::min<int64_t>(rs, (a.Ir + 255) / 256));
+  // split the contracted rows so that the grid covers the GPU, but keep >= 4
+  // rows per thread so the CTA's G x R-value reduction stays amortised;
+  // partials reduced in order
+  int64_t rs = (148 + nxy - 1) / nxy;
+  rs = std::max<int64_t>(1, std::min<int64_t>(rs, (a.Ir + 1023) / 1024));
   const int64_t chunk = (a.Ir + rs - 1) / rs;
   rs = (a.Ir + chunk - 1) / chunk;
   dim3 grid((unsigned)nxy, (unsigned)rs);
