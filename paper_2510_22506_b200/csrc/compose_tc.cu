@@ -318,8 +318,13 @@ __global__ void __launch_bounds__(THREADS, 1)
 // each slot in place and one thread TMA-stores it back as X_new, keeping a
 // few bulk groups in flight.  The bulk engines, not registers, hold the bytes
 // in flight.  Operands stream through 16-row K stages.
-constexpr int KB2 = 8;       // K rows per operand stage (one K=8 MMA step)
-constexpr int BOXB = 32 * KB2 * 4;  // bytes of one 32-row MN-major operand box
+// K rows per operand stage: 8 (one K=8 MMA step) for wide tiles; 16 or 32 for
+// narrow ones (c5: N = 64), where with K = 8 each 3-MMA stage paid a full
+// barrier / fence / commit round trip (ncu: tensor pipe 10 %, epilogue
+// waiting on the MMA 45 %)
+constexpr int KB2 = 8;
+template <int KB>
+__host__ __device__ constexpr int boxb() { return 32 * KB * 4; }  // bytes of one 32-row MN-major operand box
 constexpr int XC = 32;       // columns per X sub-tile
 constexpr int XS_DEFAULT = 9;  // X ring slots
 constexpr int XKEEP = 3;     // TMA stores allowed in flight
@@ -359,15 +364,15 @@ __device__ __forceinline__ void x_coords(const ComposeTmaArgs& a, long long t, i
 // operand ring takes whatever the X ring leaves of the 227 KB
 constexpr int T_SMEM_MAX = 232448 - 1024 /*static red[]*/;
 constexpr int T_TAIL = 1024 /*align*/ + 512 /*barriers*/;
-template <int N, bool SPLIT>
-__host__ __device__ constexpr int t_stage() { return (128 + N) * KB2 * 4 * (SPLIT ? 2 : 1); }
-template <int N, bool SPLIT, int XS>
+template <int N, bool SPLIT, int KB = KB2>
+__host__ __device__ constexpr int t_stage() { return (128 + N) * KB * 4 * (SPLIT ? 2 : 1); }
+template <int N, bool SPLIT, int XS, int KB = KB2>
 __host__ __device__ constexpr int t_ops() {
-  constexpr int o = (T_SMEM_MAX - T_TAIL - XS * (XBYTES + MBYTES)) / t_stage<N, SPLIT>();
+  constexpr int o = (T_SMEM_MAX - T_TAIL - XS * (XBYTES + MBYTES)) / t_stage<N, SPLIT, KB>();
   return o > 8 ? 8 : o;
 }
 
-template <int N, bool SPLIT, int XS>
+template <int N, bool SPLIT, int XS, int KB>
 __global__ void __launch_bounds__(T_THREADS, 1)
     k_compose_tma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmAl,
                   const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUtensorMap tmBl,
@@ -375,10 +380,11 @@ __global__ void __launch_bounds__(T_THREADS, 1)
                   const __grid_constant__ CUtensorMap tmMask, const ComposeTmaArgs args) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  constexpr uint32_t A_B = 128u * KB2 * 4u, B_B = (uint32_t)N * KB2 * 4u;
+  constexpr uint32_t A_B = 128u * KB * 4u, B_B = (uint32_t)N * KB * 4u;
+  constexpr int BOXB = boxb<KB>();
   constexpr uint32_t HI = A_B + B_B;
   constexpr uint32_t STAGE = HI * (SPLIT ? 2 : 1);
-  constexpr int OPS = t_ops<N, SPLIT, XS>();
+  constexpr int OPS = t_ops<N, SPLIT, XS, KB>();
   static_assert(OPS >= 2, "operand ring");
   uint8_t* xring = smem + OPS * STAGE;
   uint32_t* mring = reinterpret_cast<uint32_t*>(xring + XS * XBYTES);  // [XS][XC][4] mask words
@@ -436,23 +442,23 @@ __global__ void __launch_bounds__(T_THREADS, 1)
         tc::mbar_expect_tx(&full[s], tx);
         uint8_t* st = smem + s * STAGE;
         if (args.op3d) {  // box [32 rows, KB2, chunks] lands as chunk-major 1 KB boxes
-          tc::tma_load_3d(st, &tmA, &full[s], 0, kb * KB2, r0 / 32);
-          tc::tma_load_3d(st + A_B, &tmB, &full[s], 0, kb * KB2, c0 / 32);
-          if (SPLIT && args.a_pre) tc::tma_load_3d(st + HI, &tmAl, &full[s], 0, kb * KB2, r0 / 32);
-          if (SPLIT && args.b_pre) tc::tma_load_3d(st + HI + A_B, &tmBl, &full[s], 0, kb * KB2, c0 / 32);
+          tc::tma_load_3d(st, &tmA, &full[s], 0, kb * KB, r0 / 32);
+          tc::tma_load_3d(st + A_B, &tmB, &full[s], 0, kb * KB, c0 / 32);
+          if (SPLIT && args.a_pre) tc::tma_load_3d(st + HI, &tmAl, &full[s], 0, kb * KB, r0 / 32);
+          if (SPLIT && args.b_pre) tc::tma_load_3d(st + HI + A_B, &tmBl, &full[s], 0, kb * KB, c0 / 32);
         } else {
 #pragma unroll
-          for (int c = 0; c < 4; ++c) tc::tma_load_2d(st + c * BOXB, &tmA, &full[s], r0 + 32 * c, kb * KB2);
+          for (int c = 0; c < 4; ++c) tc::tma_load_2d(st + c * BOXB, &tmA, &full[s], r0 + 32 * c, kb * KB);
 #pragma unroll
           for (int c = 0; c < N / 32; ++c)
-            tc::tma_load_2d(st + A_B + c * BOXB, &tmB, &full[s], c0 + 32 * c, kb * KB2);
+            tc::tma_load_2d(st + A_B + c * BOXB, &tmB, &full[s], c0 + 32 * c, kb * KB);
           if (SPLIT && args.a_pre)
 #pragma unroll
-            for (int c = 0; c < 4; ++c) tc::tma_load_2d(st + HI + c * BOXB, &tmAl, &full[s], r0 + 32 * c, kb * KB2);
+            for (int c = 0; c < 4; ++c) tc::tma_load_2d(st + HI + c * BOXB, &tmAl, &full[s], r0 + 32 * c, kb * KB);
           if (SPLIT && args.b_pre)
 #pragma unroll
             for (int c = 0; c < N / 32; ++c)
-              tc::tma_load_2d(st + HI + A_B + c * BOXB, &tmBl, &full[s], c0 + 32 * c, kb * KB2);
+              tc::tma_load_2d(st + HI + A_B + c * BOXB, &tmBl, &full[s], c0 + 32 * c, kb * KB);
         }
       }
     }
@@ -488,7 +494,7 @@ __global__ void __launch_bounds__(T_THREADS, 1)
         tc::fence_after_sync();
         const uint32_t a = tc::smem_u32(smem + s * STAGE), b = a + A_B;
 #pragma unroll
-        for (int kk = 0; kk < KB2 / 8; ++kk) {
+        for (int kk = 0; kk < KB / 8; ++kk) {
           const uint64_t ad = tc::sdesc(a + kk * 1024, BOXB, 512, 1);
           const uint64_t bd = tc::sdesc(b + kk * 1024, BOXB, 512, 1);
           const uint32_t first = (kb | kk) != 0;
@@ -626,10 +632,10 @@ __global__ void __launch_bounds__(T_THREADS, 1)
   }
 }
 
-template <int N, bool SPLIT, int XS>
+template <int N, bool SPLIT, int XS, int KB>
 int go_tma_xs(const CUtensorMap* maps, const ComposeTmaArgs& a, int grid, cudaStream_t st) {
-  const int smem = t_ops<N, SPLIT, XS>() * t_stage<N, SPLIT>() + XS * (XBYTES + MBYTES) + T_TAIL;
-  auto fn = k_compose_tma<N, SPLIT, XS>;
+  const int smem = t_ops<N, SPLIT, XS, KB>() * t_stage<N, SPLIT, KB>() + XS * (XBYTES + MBYTES) + T_TAIL;
+  auto fn = k_compose_tma<N, SPLIT, XS, KB>;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) throw std::runtime_error(std::string("compose_tma smem: ") + cudaGetErrorString(e));
   fn<<<grid, T_THREADS, smem, st>>>(maps[0], maps[1], maps[2], maps[3], maps[4], maps[5], maps[6], a);
@@ -647,12 +653,28 @@ int compose_xs() {
   return v;
 }
 
+// K rows per operand stage for an N-wide tile (FCTN_COMPOSE_KB overrides for N = 64)
+int compose_kb(int N) {
+  static const int env = [] {
+    const char* e = getenv("FCTN_COMPOSE_KB");
+    const int x = e ? atoi(e) : 0;
+    return (x == 8 || x == 16 || x == 32) ? x : 0;
+  }();
+  if (N != 64) return KB2;
+  return env ? env : 16;
+}
+
 template <int N, bool SPLIT>
 int go_tma(const CUtensorMap* maps, const ComposeTmaArgs& a, int grid, cudaStream_t st) {
+  if constexpr (N == 64) {
+    const int kb = compose_kb(N);
+    if (kb == 16) return go_tma_xs<N, SPLIT, 5, 16>(maps, a, grid, st);
+    if (kb == 32) return go_tma_xs<N, SPLIT, 5, 32>(maps, a, grid, st);
+  }
   switch (compose_xs()) {
-    case 5: return go_tma_xs<N, SPLIT, 5>(maps, a, grid, st);
-    case 7: return go_tma_xs<N, SPLIT, 7>(maps, a, grid, st);
-    default: return go_tma_xs<N, SPLIT, 9>(maps, a, grid, st);
+    case 5: return go_tma_xs<N, SPLIT, 5, KB2>(maps, a, grid, st);
+    case 7: return go_tma_xs<N, SPLIT, 7, KB2>(maps, a, grid, st);
+    default: return go_tma_xs<N, SPLIT, 9, KB2>(maps, a, grid, st);
   }
 }
 
@@ -755,7 +777,9 @@ int launch_compose_tc(const ComposeOperands& op, const float* Xo, const uint32_t
     t.P = P;
     t.PI = P * I;
     t.I = I;
-    t.nkb = (int)((S + KB2 - 1) / KB2);
+    if (N % XC != 0) N = (N + XC - 1) / XC * XC;
+    const uint32_t kbr = (uint32_t)compose_kb(N);  // K rows per operand stage
+    t.nkb = (int)((S + kbr - 1) / kbr);
     t.rows_are_p = a.rows_are_p;
     t.a_pre = a.a_pre;
     t.b_pre = a.b_pre;
@@ -770,11 +794,11 @@ int launch_compose_tc(const ComposeOperands& op, const float* Xo, const uint32_t
     auto mk = [&](const float* base, int64_t ext, uint32_t nb) {
       if (t.op3d) {
         uint64_t d[3] = {32, (uint64_t)S, (uint64_t)(ext / 32)}, sd[2] = {(uint64_t)ext * 4, 128};
-        uint32_t b[3] = {32, KB2, nb};
+        uint32_t b[3] = {32, kbr, nb};
         return tc_make_map_f32(base, 3, d, sd, b, true);
       }
       uint64_t d[2] = {(uint64_t)ext, (uint64_t)S}, sd[1] = {(uint64_t)ext * 4};
-      uint32_t b[2] = {32, KB2};
+      uint32_t b[2] = {32, kbr};
       return tc_make_map_f32(base, 2, d, sd, b, true);
     };
     CUtensorMap tM = mk(Mh, p, nb_m);
