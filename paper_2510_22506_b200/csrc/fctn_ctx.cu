@@ -985,13 +985,13 @@ class Ctx : public Executor {
     launch_chol_solve(G, S, dp.H1, mu[k], Fr, Fi, check_mu[k], dstatus, st);
     pend(pm, 8.0 * (S * S + 4.0 * dp.H1 * S), 1);
     pm = pbegin(FCTN_K_DFT);
-    if (dtype == FCTN_F64)
-      launch_dft_inv<double>(Fr, Fi, dp, S, cosT[k], sinT[k], A64[k], Ascratch, nullptr, extrap, alpha, beta,
-                             delta[k], sgn, colstats, st);
-    else
-      launch_dft_inv<float>(Fr, Fi, dp, S, cosT[k], sinT[k], A64[k], Ascratch, (float*)Ac[k], extrap, alpha, beta,
-                            delta[k], sgn, colstats, st);
-    pend(pm, 8.0 * (3.0 * I * S + 2.0 * dp.H1 * S), 1);
+    const int ninv = dtype == FCTN_F64
+                         ? launch_dft_inv<double>(Fr, Fi, dp, S, cosT[k], sinT[k], A64[k], Ascratch, nullptr, extrap,
+                                                  alpha, beta, delta[k], sgn, colstats, st)
+                         : launch_dft_inv<float>(Fr, Fi, dp, S, cosT[k], sinT[k], A64[k], Ascratch, (float*)Ac[k],
+                                                 extrap, alpha, beta, delta[k], sgn, colstats, st);
+    launches += ninv - 1;
+    pend(pm, 8.0 * (3.0 * I * S + 2.0 * dp.H1 * S), ninv);
     pm = pbegin(FCTN_K_FGRAM);
     launch_factor_gram(Ascratch, I, S, epart, E64[k], colstats, dstats + 3 * k, st);
     pend(pm, 8.0 * (I * S + S * S), 2);

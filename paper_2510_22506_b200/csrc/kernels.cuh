@@ -123,7 +123,7 @@ void launch_chol_solve(const double* G, int64_t S, int64_t H1, const double* mu,
 // inverse DFT + extrapolation + factor write + per-column stats
 // (solver.py:240-243,330-333; laplacian.py:59-71)
 template <typename T>
-void launch_dft_inv(const double* Fr, const double* Fi, const DftPlan& p, int64_t S, const double* cosT,
+int launch_dft_inv(const double* Fr, const double* Fi, const DftPlan& p, int64_t S, const double* cosT,
                     const double* sinT, const double* Aold, double* Anew, T* Acompute, int extrap, double alpha,
                     double beta, double delta, double sgn, double* colstats, cudaStream_t st);
 // per-column [0, ||a||^2, a.(L a)] without a previous iterate

@@ -171,3 +171,23 @@ def test_gpu_fp32_tc_join_on_every_contraction(name, dims, kmajor):
         env["FCTN_TC_JOIN_KMAJOR"] = "1"
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
+
+
+@pytest.mark.parametrize("dims,rank", [((600, 20, 6), 2), ((1024, 8, 5), 3), ((520, 6, 4, 3), 2)])
+def test_gpu_split_dft_fp64(dims, rank):
+    """Long modes (I >= 512) with few bond columns run each column's DFT on
+    several CTAs (w1 residue classes) and the inverse's column statistics in
+    a separate kernel: FP64 parity with the oracle (incl. the objective, which
+    uses those statistics) and extrapolation on."""
+    rng = np.random.default_rng(5)
+    truth = np.cumsum(rng.standard_normal(dims), axis=0) / 10.0
+    from paper_2510_22506_b200.workloads import sample_mask
+    mask = sample_mask(dims, 0.3, 5)
+    kw = dict(lam=0.35, delta=0.5, rho=0.1, eps=0.0, max_iters=4, max_rank=rank, initial_rank=rank,
+              rank_policy="fixed", algorithm="afctnlr", shuffle=True, seed=1, extrapolation=(0.5, 0.5))
+    ref = O.run(np.where(mask, truth, 0.0), mask, **kw)
+    res = P.run(P.Observation(truth, mask), P.SolverConfig(**kw))
+    assert rel(res.x, ref.x) <= FP64_TOL
+    for a, b in zip(res.trace, ref.trace):
+        assert a.objective == pytest.approx(b.objective, rel=FP64_TOL)
+        assert a.step_sq == pytest.approx(b.step_sq, rel=1e-6, abs=1e-12)
