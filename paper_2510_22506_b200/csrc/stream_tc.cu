@@ -380,6 +380,172 @@ __global__ void __launch_bounds__(TS_THREADS, 1)
   }
 }
 
+// Swapped-role form for short modes (I <= 64 < S <= 128, X tile K-major; c5's
+// 48 x 81 products): the bond rows s of the M_k tile are the MMA's M side
+// (A, split into TMEM by the converters) and the X rows the N side (B, split
+// in place in shared memory, the low half written into the tile's unused rows
+// NI..2NI-1 so [X hi | X lo] is one N-doubled operand).  The MMA then spends
+// 128 x 3NI instead of 128 x 3S' per K step with only 48 of its 128 rows live
+// (ncu, k_stream_ts at c5: tensor pipe 58 % with I = 48).  Partials are
+// written in the same [split][i + I s] layout.
+template <int NT, int NI>
+struct TswSmem {
+  static constexpr int X_BYTES = A_BYTES;         // 128 X rows (TMA box), hi in 0..NI-1, lo in NI..2NI-1
+  static constexpr int M_BYTES = NT * BK * 4;     // NT bond rows
+  static constexpr int STAGE_BYTES = X_BYTES + M_BYTES;
+  static constexpr int ACC = 2 * NI;
+  static constexpr int S_SMEM = (200 * 1024) / STAGE_BYTES > 6 ? 6 : (200 * 1024) / STAGE_BYTES;
+  static constexpr int S_TMEM = (512 - ACC) / 64 > 6 ? 6 : (512 - ACC) / 64;
+  static constexpr int STAGES = S_SMEM < S_TMEM ? S_SMEM : S_TMEM;
+  static constexpr int TOTAL = STAGES * STAGE_BYTES + 1024 + 256;
+};
+
+template <int NT, int NI>
+__global__ void __launch_bounds__(TS_THREADS, 1)
+    k_stream_tsw(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmM,
+                 float* __restrict__ part, int I, int S, long long nkb_total, long long kb_per_split, int nPB) {
+  using L = TswSmem<NT, NI>;
+  constexpr int STAGES = L::STAGES;
+  static_assert(STAGES >= 2 && NI % 16 == 0 && 2 * NI <= 128, "tsw shape");
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * L::STAGE_BYTES);
+  uint64_t* conv = full + STAGES;
+  uint64_t* empty = conv + STAGES;
+  uint64_t* tmem_full = empty + STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long split = blockIdx.y;
+  const long long kb0 = split * kb_per_split;
+  long long kb1 = kb0 + kb_per_split;
+  if (kb1 > nkb_total) kb1 = nkb_total;
+  const int nkb = (int)(kb1 - kb0);
+
+  if (warp == 0 && lane == 0) {
+    tc::tma_prefetch(&tmX);
+    tc::tma_prefetch(&tmM);
+    for (int s = 0; s < STAGES; ++s) {
+      tc::mbar_init(&full[s], 1);
+      tc::mbar_init(&conv[s], TS_CONV_WARPS);
+      tc::mbar_init(&empty[s], 1);
+    }
+    tc::mbar_init(tmem_full, 1);
+    tc::fence_barrier_init();
+  }
+  if (warp == 1) tc::tmem_alloc<512>(tmem_slot);
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0 && lane == 0) {
+    // ---------------- TMA producer: X tile [128 i rows x 32 p] + M tile [NT s rows x 32 p]
+    for (int it = 0; it < nkb; ++it) {
+      const int s = it % STAGES;
+      tc::mbar_wait(&empty[s], ((it / STAGES) & 1) ^ 1);
+      tc::mbar_expect_tx(&full[s], L::X_BYTES + L::M_BYTES);
+      const long long kb = kb0 + it;
+      uint8_t* a = smem + s * L::STAGE_BYTES;
+      const int pb = (int)(kb % nPB) * BK;
+      const int q = (int)(kb / nPB);
+      tc::tma_load_3d(a, &tmX, &full[s], pb, 0, q);
+      tc::tma_load_3d(a + L::X_BYTES, &tmM, &full[s], pb, q, 0);
+    }
+  } else if (warp == 1 && lane == 0) {
+    // ---------------- MMA issuer: D[s, 0:2NI] = A_hi [X_hi | X_lo]^T, D[s, 0:NI] += A_lo X_hi^T
+    constexpr uint32_t idesc2 = tc::idesc_tf32(128, 2 * NI, false, false);
+    constexpr uint32_t idesc1 = tc::idesc_tf32(128, NI, false, false);
+    for (int it = 0; it < nkb; ++it) {
+      const int s = it % STAGES;
+      tc::mbar_wait(&conv[s], (it / STAGES) & 1);
+      tc::fence_after_sync();
+      const uint32_t x = tc::smem_u32(smem + s * L::STAGE_BYTES);
+      const uint32_t ahi = tmem + L::ACC + 64 * s, alo = ahi + 32;
+#pragma unroll
+      for (int kk = 0; kk < BK / 8; ++kk) {
+        const uint64_t bd = tc::sdesc(x + kk * 32, 16, 1024);  // rows 0..2NI-1 = [X hi | X lo]
+        tc::mma_tf32_ts(tmem, ahi + 8 * kk, bd, idesc2, (it | kk) != 0);
+        tc::mma_tf32_ts(tmem, alo + 8 * kk, bd, idesc1, 1);
+      }
+      tc::mma_commit(&empty[s]);
+    }
+    tc::mma_commit(tmem_full);
+  } else if (warp >= 2) {
+    // ---------------- M tile split into TMEM (lane = s), X rows split in place
+    const int q = warp & 3;
+    const int hf = (warp - 2) >> 2;
+    const int row = 32 * q + lane;   // bond row s
+    const int ct = threadIdx.x - 64;  // 0..255
+    for (int it = 0; it < nkb; ++it) {
+      const int s = it % STAGES;
+      tc::mbar_wait(&full[s], (it / STAGES) & 1);
+      uint8_t* a = smem + s * L::STAGE_BYTES;
+      if (32 * q < NT) {  // quadrants past the M tile hold no bond row (D rows never stored)
+        float x[16];
+        const uint8_t* mrow = a + L::X_BYTES + (row < NT ? row : 0) * 128;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const float4 v = tc::lds128(tc::smem_u32(mrow) + 16u * (uint32_t)((4 * hf + c) ^ (row & 7)));
+          x[4 * c] = v.x;
+          x[4 * c + 1] = v.y;
+          x[4 * c + 2] = v.z;
+          x[4 * c + 3] = v.w;
+        }
+        float lo[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const float h = tc::tf32_rn_int(x[j]);
+          lo[j] = tc::tf32_rn_int(x[j] - h);
+          x[j] = h;
+        }
+        const uint32_t ta = tmem + ((uint32_t)(32 * q) << 16) + L::ACC + 64 * s + 16 * hf;
+        tc::tmem_st16(ta, x);
+        tc::tmem_st16(ta + 32, lo);
+      }
+      // X rows 0..NI-1: hi in place, lo into row + NI (same swizzle phase: NI % 8 == 0)
+      const uint32_t xs = tc::smem_u32(a);
+      for (int e = ct; e < NI * 8; e += 32 * TS_CONV_WARPS) {
+        const int r = e >> 3, c = e & 7;
+        const uint32_t off = (uint32_t)(r * 128) + 16u * (uint32_t)(c ^ (r & 7));
+        const float4 v = tc::lds128(xs + off);
+        const float4 h = make_float4(tc::tf32_rn_int(v.x), tc::tf32_rn_int(v.y), tc::tf32_rn_int(v.z), tc::tf32_rn_int(v.w));
+        tc::sts128(xs + off, h);
+        tc::sts128(xs + off + (uint32_t)(NI * 128), make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w));
+      }
+      tc::fence_proxy_async_smem();
+      tc::tmem_wait_st();
+      tc::fence_before_sync();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&conv[s]);
+    }
+    tc::mbar_wait(tmem_full, 0);
+    tc::fence_after_sync();
+    float* out = part + split * (long long)I * S;
+    if (32 * q < NT) {
+#pragma unroll 1
+      for (int c0 = 16 * hf; c0 < NI; c0 += 32) {
+        float v[16], w[16];
+        tc::tmem_ld16(tmem + ((uint32_t)(32 * q) << 16) + c0, v);
+        tc::tmem_ld16(tmem + ((uint32_t)(32 * q) << 16) + NI + c0, w);
+        if (row < S) {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const int i = c0 + j;
+            if (i < I) out[i + (long long)I * row] = v[j] + w[j];
+          }
+        }
+      }
+    }
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  if (warp == 1) {
+    tc::fence_after_sync();
+    tc::tmem_dealloc<512>(tmem);
+  }
+}
+
 // Persistent form of k_stream_ts for unsplit products with many row tiles
 // (the Z_j passes): one CTA per SM walks its row tiles with one continuous
 // operand pipeline; two TMEM accumulators let four epilogue warps drain tile
@@ -723,6 +889,19 @@ TcStreamPlan plan_stream_tc(int64_t I, int64_t P, int64_t Q, int64_t S, int n_sm
   return tp;
 }
 
+template <int NT, int NI>
+static void go_tsw(const CUtensorMap& mx, const CUtensorMap& mm, float* part, int64_t I, int64_t S,
+                   const TcStreamPlan& tp, cudaStream_t st) {
+  const int smem = TswSmem<NT, NI>::TOTAL;
+  auto fn = k_stream_tsw<NT, NI>;
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) throw std::runtime_error(std::string("stream_tsw smem: ") + cudaGetErrorString(e));
+  fn<<<dim3(1u, (unsigned)tp.nsplit), TS_THREADS, smem, st>>>(mx, mm, part, (int)I, (int)S, tp.nkb, tp.kb_per_split,
+                                                              (int)tp.npb);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) throw std::runtime_error(std::string("stream_tsw: ") + cudaGetErrorString(e));
+}
+
 void launch_stream_tc(const float* X, const float* M, float* part, int64_t I, int64_t P, int64_t Q, int64_t S,
                       const TcStreamPlan& tp, cudaStream_t st, const float* Mlo) {
   CUtensorMap mx, mx3, mm, mml;
@@ -753,6 +932,21 @@ void launch_stream_tc(const float* X, const float* M, float* part, int64_t I, in
     mml = b_pre ? make_map(Mlo, 3, dm, sm, bm) : mm;
   }
   const bool amn = P == 1;
+  // short mode (I <= 64) against many bond columns: the swapped-role kernel
+  static const bool no_tsw = getenv("FCTN_NO_TSW") != nullptr;
+  if (!amn && !b_pre && tp.split3 && !no_tsw && I <= 64 && S > I && tp.nt >= 96 && tp.n_mtiles == 1) {
+    const int ni = I <= 32 ? 32 : I <= 48 ? 48 : 64;
+    if (tp.nt == 96) {
+      if (ni == 32) go_tsw<96, 32>(mx, mm, part, I, S, tp, st);
+      else if (ni == 48) go_tsw<96, 48>(mx, mm, part, I, S, tp, st);
+      else go_tsw<96, 64>(mx, mm, part, I, S, tp, st);
+    } else {
+      if (ni == 32) go_tsw<128, 32>(mx, mm, part, I, S, tp, st);
+      else if (ni == 48) go_tsw<128, 48>(mx, mm, part, I, S, tp, st);
+      else go_tsw<128, 64>(mx, mm, part, I, S, tp, st);
+    }
+    return;
+  }
   switch (tp.nt) {
     case 32: amn ? go<32, true>(mx, mx3, mm, mml, b_pre, x3d, part, I, S, tp, st) : go<32, false>(mx, mx3, mm, mml, b_pre, x3d, part, I, S, tp, st); break;
     case 64: amn ? go<64, true>(mx, mx3, mm, mml, b_pre, x3d, part, I, S, tp, st) : go<64, false>(mx, mx3, mm, mml, b_pre, x3d, part, I, S, tp, st); break;
