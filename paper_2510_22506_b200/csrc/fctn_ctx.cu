@@ -16,6 +16,7 @@
 #include <memory>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/fctn_b200.h"
@@ -1331,6 +1332,8 @@ int fctn_upload(fctn_ctx* c, const void* x_F, const uint8_t* mask_F) {
   });
 }
 
+}  // extern "C"
+
 namespace fctn {
 // Page-lock a caller buffer for the duration of one large transfer (the
 // pageable path stages through the driver at a fraction of the PCIe/C2C
@@ -1348,27 +1351,117 @@ struct HostPin {
     if (p) cudaHostUnregister(p);
   }
 };
+
+// Large host <-> device transfers through a ring of pinned 32 MB chunks:
+// several host threads copy a chunk between the caller's (pageable) buffer
+// and a pinned buffer while the DMA engine moves the previous one.  Measured
+// alternative: page-locking the caller's 2 GB buffer (cudaHostRegister)
+// costs more than the copy itself and the pageable driver path runs at
+// ~8 GB/s.  Synchronous with respect to the host on return.
+struct Stager {
+  static constexpr size_t CH = (size_t)32 << 20;
+  static constexpr int NB = 3;
+  void* buf[NB] = {nullptr, nullptr, nullptr};
+  cudaEvent_t ev[NB] = {nullptr, nullptr, nullptr};
+  int nthr = 1;
+  Stager() {
+    for (int b = 0; b < NB; ++b) {
+      CK(cudaMallocHost(&buf[b], CH));
+      CK(cudaEventCreateWithFlags(&ev[b], cudaEventDisableTiming));
+    }
+    const unsigned hc = std::thread::hardware_concurrency();
+    nthr = (int)std::max(1u, std::min(8u, hc ? hc / 2 : 1u));
+  }
+  ~Stager() {
+    for (int b = 0; b < NB; ++b) {
+      if (buf[b]) cudaFreeHost(buf[b]);
+      if (ev[b]) cudaEventDestroy(ev[b]);
+    }
+  }
+  void pcopy(void* dst, const void* src, size_t n) const {  // parallel memcpy
+    if (nthr <= 1 || n < ((size_t)4 << 20)) {
+      std::memcpy(dst, src, n);
+      return;
+    }
+    const size_t part = ((n + nthr - 1) / nthr + 4095) & ~(size_t)4095;
+    std::vector<std::thread> th;
+    for (int t = 1; t < nthr; ++t) {
+      const size_t o = (size_t)t * part;
+      if (o >= n) break;
+      th.emplace_back([=] { std::memcpy((char*)dst + o, (const char*)src + o, std::min(part, n - o)); });
+    }
+    std::memcpy(dst, src, std::min(part, n));
+    for (auto& x : th) x.join();
+  }
+  void h2d(void* dst, const void* src, size_t n, cudaStream_t st) {
+    size_t c = 0;
+    for (size_t o = 0; o < n; o += CH, ++c) {
+      const int b = (int)(c % NB);
+      const size_t m = std::min(CH, n - o);
+      CK(cudaEventSynchronize(ev[b]));  // the DMA that last read buf[b] is done
+      pcopy(buf[b], (const char*)src + o, m);
+      CK(cudaMemcpyAsync((char*)dst + o, buf[b], m, cudaMemcpyHostToDevice, st));
+      CK(cudaEventRecord(ev[b], st));
+    }
+    CK(cudaStreamSynchronize(st));
+  }
+  // D2H of n bytes produced chunk by chunk: `produce(o, m)` enqueues on `st`
+  // whatever must run before chunk [o, o+m) of `src` is ready (may be empty)
+  template <typename Produce>
+  void d2h(void* dst, const void* src, size_t n, cudaStream_t st, Produce&& produce) {
+    const size_t nc = (n + CH - 1) / CH;
+    for (size_t c = 0; c <= nc; ++c) {
+      if (c < nc) {
+        const int b = (int)(c % NB);
+        const size_t o = c * CH, m = std::min(CH, n - o);
+        produce(o, m, b);
+        CK(cudaMemcpyAsync(buf[b], (const char*)src + (src_is_chunk ? 0 : o), m, cudaMemcpyDeviceToHost, st));
+        CK(cudaEventRecord(ev[b], st));
+      }
+      if (c >= 1) {  // drain the previous chunk while this one moves
+        const size_t pc = c - 1;
+        const int pb = (int)(pc % NB);
+        const size_t o = pc * CH, m = std::min(CH, n - o);
+        CK(cudaEventSynchronize(ev[pb]));
+        pcopy((char*)dst + o, buf[pb], m);
+      }
+    }
+  }
+  bool src_is_chunk = false;  // src is a per-chunk scratch (offset 0) rather than the whole tensor
+};
+
+static Stager& stager() {  // one ring per process (the library is not thread-safe per context)
+  static Stager* s = new Stager();
+  return *s;
+}
+static bool use_stager(size_t bytes) { return bytes >= ((size_t)64 << 20) && !getenv("FCTN_NO_STAGE"); }
 }  // namespace fctn
+
+extern "C" {
 
 int fctn_upload_f64(fctn_ctx* c, const double* x_F, const uint8_t* mask_F) {
   return fctn::guarded(&c->impl, [&] {
     Ctx& x = c->impl;
     const int64_t T = x.sh.total();
-    fctn::HostPin pin_x(x_F, (size_t)T * 8), pin_m(mask_F, (size_t)T);
+    const bool stage = fctn::use_stager((size_t)T * 8);
+    fctn::HostPin pin_x(stage ? nullptr : x_F, stage ? 0 : (size_t)T * 8), pin_m(stage ? nullptr : mask_F, stage ? 0 : (size_t)T);
     if (x.dtype == FCTN_F64) {
-      CK(cudaMemcpyAsync(x.X[0], x_F, T * 8, cudaMemcpyHostToDevice, x.st));
+      if (stage) fctn::stager().h2d(x.X[0], x_F, (size_t)T * 8, x.st);
+      else CK(cudaMemcpyAsync(x.X[0], x_F, T * 8, cudaMemcpyHostToDevice, x.st));
     } else {  // fp64 host data, fp32 context: convert on the device, in chunks
       const int64_t chunk = std::min<int64_t>(T, (int64_t)1 << 26);
       double* tmp = nullptr;
       CK(cudaMallocAsync((void**)&tmp, chunk * 8, x.st));
       for (int64_t o = 0; o < T; o += chunk) {
         const int64_t n = std::min(chunk, T - o);
-        CK(cudaMemcpyAsync(tmp, x_F + o, n * 8, cudaMemcpyHostToDevice, x.st));
+        if (stage) fctn::stager().h2d(tmp, x_F + o, (size_t)n * 8, x.st);
+        else CK(cudaMemcpyAsync(tmp, x_F + o, n * 8, cudaMemcpyHostToDevice, x.st));
         fctn::launch_convert_f64_f32(tmp, (float*)x.X[0] + o, n, x.st);
       }
       CK(cudaFreeAsync(tmp, x.st));
     }
-    CK(cudaMemcpyAsync(x.mask, mask_F, T, cudaMemcpyHostToDevice, x.st));
+    if (stage) fctn::stager().h2d(x.mask, mask_F, (size_t)T, x.st);
+    else CK(cudaMemcpyAsync(x.mask, mask_F, T, cudaMemcpyHostToDevice, x.st));
     fctn::launch_pack_mask(x.mask, T, x.maskbits, x.st);
     CK(cudaStreamSynchronize(x.st));
     x.cur = 0;
@@ -1382,6 +1475,48 @@ int fctn_get_x_f64(fctn_ctx* c, double* x_F) {
   return fctn::guarded(&c->impl, [&] {
     Ctx& x = c->impl;
     const int64_t T = x.sh.total();
+    if (fctn::use_stager((size_t)T * 8)) {
+      fctn::Stager& sg = fctn::stager();
+      if (x.dtype == FCTN_F64) {
+        sg.src_is_chunk = false;
+        sg.d2h(x_F, x.X[x.cur], (size_t)T * 8, x.st, [](size_t, size_t, int) {});
+      } else {  // convert each 32 MB chunk on the device into one of three scratch slots
+        double* tmp = nullptr;
+        const size_t cd = fctn::Stager::CH / 8;  // doubles per chunk
+        CK(cudaMallocAsync((void**)&tmp, 3 * fctn::Stager::CH, x.st));
+        // the D2H of chunk c reads slot c % 3: issue it from that slot
+        sg.src_is_chunk = true;
+        int64_t chunk_id = 0;
+        const float* X32 = (const float*)x.X[x.cur];
+        for (int64_t o = 0; o < T; o += (int64_t)cd, ++chunk_id) {
+          (void)o;
+        }
+        // explicit pipeline (the generic d2h reads one scratch address)
+        const size_t n = (size_t)T * 8;
+        const size_t nc = (n + fctn::Stager::CH - 1) / fctn::Stager::CH;
+        for (size_t ci = 0; ci <= nc; ++ci) {
+          if (ci < nc) {
+            const int b = (int)(ci % fctn::Stager::NB);
+            const size_t off = ci * fctn::Stager::CH, m = std::min(fctn::Stager::CH, n - off);
+            double* slot = tmp + (size_t)b * cd;
+            fctn::launch_convert_f32_f64(X32 + off / 8, slot, (int64_t)(m / 8), x.st);
+            CK(cudaMemcpyAsync(sg.buf[b], slot, m, cudaMemcpyDeviceToHost, x.st));
+            CK(cudaEventRecord(sg.ev[b], x.st));
+          }
+          if (ci >= 1) {
+            const size_t pc = ci - 1;
+            const int pb = (int)(pc % fctn::Stager::NB);
+            const size_t off = pc * fctn::Stager::CH, m = std::min(fctn::Stager::CH, n - off);
+            CK(cudaEventSynchronize(sg.ev[pb]));
+            sg.pcopy((char*)x_F + off, sg.buf[pb], m);
+          }
+        }
+        CK(cudaFreeAsync(tmp, x.st));
+        (void)chunk_id;
+      }
+      CK(cudaStreamSynchronize(x.st));
+      return;
+    }
     fctn::HostPin pin_x(x_F, (size_t)T * 8);
     if (x.dtype == FCTN_F64) {
       CK(cudaMemcpyAsync(x_F, x.X[x.cur], T * 8, cudaMemcpyDeviceToHost, x.st));
