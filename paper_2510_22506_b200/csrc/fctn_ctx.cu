@@ -1910,15 +1910,18 @@ int fctn_quality(int device, int dtype, int n, const int64_t* dims, const void* 
       cudaStream_t s;
       ~StreamGuard() { cudaStreamDestroy(s); }
     } sg{st};
-    fctn::HostPin pe(est_F, T * es), pt(truth_F, T * es);
     void *de = nullptr, *dt = nullptr;
     uint8_t* dm = nullptr;
     CK(cudaMallocAsync(&de, T * es, st));
     CK(cudaMallocAsync(&dt, T * es, st));
     if (mask_F) CK(cudaMallocAsync((void**)&dm, T, st));
-    CK(cudaMemcpyAsync(de, est_F, T * es, cudaMemcpyHostToDevice, st));
-    CK(cudaMemcpyAsync(dt, truth_F, T * es, cudaMemcpyHostToDevice, st));
-    if (mask_F) CK(cudaMemcpyAsync(dm, mask_F, T, cudaMemcpyHostToDevice, st));
+    auto up = [&](void* d, const void* h, size_t n) {
+      if (fctn::use_stager(n)) fctn::stager().h2d(d, h, n, st);
+      else CK(cudaMemcpyAsync(d, h, n, cudaMemcpyHostToDevice, st));
+    };
+    up(de, est_F, T * es);
+    up(dt, truth_F, T * es);
+    if (mask_F) up(dm, mask_F, T);
     fctn::quality_dispatch(dtype, dtype, hw, hw, T / hw, n_sm, de, dt, dm, peak, [](double*, int64_t) {}, out, st);
     CK(cudaFreeAsync(de, st));
     CK(cudaFreeAsync(dt, st));
@@ -1937,10 +1940,10 @@ int fctn_quality_ctx(fctn_ctx* c, const void* truth_F, int truth_dtype, int mask
     const size_t es = truth_dtype == FCTN_F64 ? 8 : 4;
     const int64_t hw_local = x.sh.dims[0] * x.sh.dims[1];
     const int64_t hw_global = x.gsh.dims[0] * x.gsh.dims[1];
-    fctn::HostPin pt(truth_F, T * es);
     void* dt = nullptr;
     CK(cudaMallocAsync(&dt, T * es, x.st));
-    CK(cudaMemcpyAsync(dt, truth_F, T * es, cudaMemcpyHostToDevice, x.st));
+    if (fctn::use_stager(T * es)) fctn::stager().h2d(dt, truth_F, T * es, x.st);
+    else CK(cudaMemcpyAsync(dt, truth_F, T * es, cudaMemcpyHostToDevice, x.st));
     fctn::quality_dispatch(x.dtype, truth_dtype, hw_local, hw_global, T / hw_local, x.n_sm, x.X[x.cur], dt,
                            mask_mode ? x.mask : nullptr, peak,
                            [&](double* d, int64_t nd) { x.allreduce_sum(d, nd); }, out, x.st);
