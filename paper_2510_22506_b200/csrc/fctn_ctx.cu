@@ -881,15 +881,14 @@ class Ctx : public Executor {
     // sharded: Y_0 rows are this slab's (all-gathered), other Y_k are this slab's share (all-reduced)
     double* yout = (sharded() && k == 0) ? yloc : Y;
     int pm = pbegin(FCTN_K_YSMALL);
+    // + rho A_prev (sylvester.py:106) folded into the final reduction (sharded: added after the all-reduce)
+    const double* ap = sharded() ? nullptr : A64[k];
     const int nl = dtype == FCTN_F32
-                       ? launch_y_from_z<float>((const float*)Zb[j], (const float*)fac_ptr(l), a, yout, ypart, st)
-                       : launch_y_from_z<double>((const double*)Zb[j], A64[l], a, yout, ypart, st);
+                       ? launch_y_from_z<float>((const float*)Zb[j], (const float*)fac_ptr(l), a, yout, ypart, ap,
+                                                rho, st)
+                       : launch_y_from_z<double>((const double*)Zb[j], A64[l], a, yout, ypart, ap, rho, st);
     launches += nl;
-    if (!sharded()) {
-      launch_axpy(Y, A64[k], rho, I * S, st);  // + rho A_prev (sylvester.py:106)
-      ++launches;
-    }
-    pend(pm, (double)esize * zsize(j) + 8.0 * I * S, nl + (sharded() ? 0 : 1));
+    pend(pm, (double)esize * zsize(j) + 8.0 * I * S, nl);
     if (sharded()) finish_y(k, k == 0);
   }
   // M_j of the current factors into Mbuf, outside the reference's chain (no meter)

@@ -518,7 +518,8 @@ void launch_axpy(double* y, const double* x, double a, int64_t n, cudaStream_t s
 // fp64 accumulation, deterministic.
 template <typename T, int RC, int RA, int G>
 __global__ void __launch_bounds__(256, 2) k_yzl(const T* __restrict__ Z, const T* __restrict__ A, YzArgs p,
-                                             double* __restrict__ Y, int64_t r_chunk) {
+                                             double* __restrict__ Y, int64_t r_chunk,
+                                             const double* __restrict__ aprev, double rho) {
   const int64_t bz = blockIdx.x % p.Rz, o0 = (blockIdx.x / p.Rz) * G;
   const int64_t rows = p.Ir * p.Io;
   const int64_t r_lo = blockIdx.y * r_chunk, r_hi = (p.Ir < r_lo + r_chunk) ? p.Ir : r_lo + r_chunk;
@@ -572,7 +573,9 @@ __global__ void __launch_bounds__(256, 2) k_yzl(const T* __restrict__ Z, const T
     if (o >= p.Io) continue;
     double v = 0.0;
     for (int q = 0; q < 8; ++q) v += red[q][e];
-    Y[o + p.Io * (bz * p.yz + c * p.ya)] = v;
+    const int64_t yi = o + p.Io * (bz * p.yz + c * p.ya);
+    if (aprev) v += rho * aprev[yi];  // + rho A_prev (sylvester.py:106), unsplit case
+    Y[yi] = v;
   }
 }
 
@@ -615,7 +618,8 @@ __global__ void __launch_bounds__(256) k_yzs(const T* __restrict__ Z, const T* _
 }
 
 template <typename T, int R>
-static int yzl_go(const T* Z, const T* Al, const YzArgs& a, double* Y, double* part, cudaStream_t st) {
+static int yzl_go(const T* Z, const T* Al, const YzArgs& a, double* Y, double* part, const double* aprev,
+                  double rho, cudaStream_t st) {
   constexpr int G = R * R > 32 ? 4 : 8;  // G x R fp64 accumulators + R x R operands stay in registers
   const int64_t nxy = a.Rz * ((a.Io + G - 1) / G);
   // split the contracted rows so that the grid covers the GPU, but keep >= 4
@@ -626,25 +630,26 @@ static int yzl_go(const T* Z, const T* Al, const YzArgs& a, double* Y, double* p
   const int64_t chunk = (a.Ir + rs - 1) / rs;
   rs = (a.Ir + chunk - 1) / chunk;
   dim3 grid((unsigned)nxy, (unsigned)rs);
-  k_yzl<T, R, R, G><<<grid, 256, 0, st>>>(Z, Al, a, rs > 1 ? part : Y, chunk);
-  if (rs > 1) launch_reduce_splits(part, (int)rs, a.Io * a.Rz * R, nullptr, 0.0, Y, st);
+  k_yzl<T, R, R, G><<<grid, 256, 0, st>>>(Z, Al, a, rs > 1 ? part : Y, chunk, rs > 1 ? nullptr : aprev, rho);
+  if (rs > 1) launch_reduce_splits(part, (int)rs, a.Io * a.Rz * R, aprev, rho, Y, st);
   return rs > 1 ? 2 : 1;
 }
 
 template <typename T>
-int launch_y_from_z(const T* Z, const T* Al, const YzArgs& a, double* Y, double* part, cudaStream_t st) {
+int launch_y_from_z(const T* Z, const T* Al, const YzArgs& a, double* Y, double* part, const double* aprev,
+                    double rho, cudaStream_t st) {
   if (a.long_l) {
     int nl = 0;
     if (a.Rc != a.Ra || a.Rc > 8) throw std::runtime_error("y_from_z: non-uniform bonds need the generic contraction");
     switch (a.Rc) {
-      case 1: nl = yzl_go<T, 1>(Z, Al, a, Y, part, st); break;
-      case 2: nl = yzl_go<T, 2>(Z, Al, a, Y, part, st); break;
-      case 3: nl = yzl_go<T, 3>(Z, Al, a, Y, part, st); break;
-      case 4: nl = yzl_go<T, 4>(Z, Al, a, Y, part, st); break;
-      case 5: nl = yzl_go<T, 5>(Z, Al, a, Y, part, st); break;
-      case 6: nl = yzl_go<T, 6>(Z, Al, a, Y, part, st); break;
-      case 7: nl = yzl_go<T, 7>(Z, Al, a, Y, part, st); break;
-      default: nl = yzl_go<T, 8>(Z, Al, a, Y, part, st); break;
+      case 1: nl = yzl_go<T, 1>(Z, Al, a, Y, part, aprev, rho, st); break;
+      case 2: nl = yzl_go<T, 2>(Z, Al, a, Y, part, aprev, rho, st); break;
+      case 3: nl = yzl_go<T, 3>(Z, Al, a, Y, part, aprev, rho, st); break;
+      case 4: nl = yzl_go<T, 4>(Z, Al, a, Y, part, aprev, rho, st); break;
+      case 5: nl = yzl_go<T, 5>(Z, Al, a, Y, part, aprev, rho, st); break;
+      case 6: nl = yzl_go<T, 6>(Z, Al, a, Y, part, aprev, rho, st); break;
+      case 7: nl = yzl_go<T, 7>(Z, Al, a, Y, part, aprev, rho, st); break;
+      default: nl = yzl_go<T, 8>(Z, Al, a, Y, part, aprev, rho, st); break;
     }
     check_launch("y_from_z_long");
     return nl;
@@ -654,11 +659,13 @@ int launch_y_from_z(const T* Z, const T* Al, const YzArgs& a, double* Y, double*
   if (a.Ra <= 8) k_yzs<T, 8><<<grid, 256, 0, st>>>(Z, Al, a, part);
   else k_yzs<T, 16><<<grid, 256, 0, st>>>(Z, Al, a, part);
   check_launch("y_from_z_short");
-  launch_reduce_splits(part, a.Rc, a.Ir * a.Rz * a.Ra, nullptr, 0.0, Y, st);
+  launch_reduce_splits(part, a.Rc, a.Ir * a.Rz * a.Ra, aprev, rho, Y, st);
   return 2;
 }
-template int launch_y_from_z<float>(const float*, const float*, const YzArgs&, double*, double*, cudaStream_t);
-template int launch_y_from_z<double>(const double*, const double*, const YzArgs&, double*, double*, cudaStream_t);
+template int launch_y_from_z<float>(const float*, const float*, const YzArgs&, double*, double*, const double*, double,
+                                    cudaStream_t);
+template int launch_y_from_z<double>(const double*, const double*, const YzArgs&, double*, double*, const double*,
+                                     double, cudaStream_t);
 
 __global__ void k_convert(const double* __restrict__ in, float* __restrict__ out, int64_t n) {
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)

@@ -56,7 +56,9 @@ struct YzArgs {
   bool long_l;
 };
 template <typename T>
-int launch_y_from_z(const T* Z, const T* Al, const YzArgs& a, double* Y, double* part, cudaStream_t st);  // launches
+// + rho * aprev when aprev != null (sylvester.py:106); returns the launches
+int launch_y_from_z(const T* Z, const T* Al, const YzArgs& a, double* Y, double* part, const double* aprev, double rho,
+                    cudaStream_t st);
 // mode-0 sharding helpers (fctn_set_comm)
 void launch_copy_rows(const double* A, int64_t I, int64_t S, int64_t lo, int64_t rows, void* out, bool f32,
                       cudaStream_t st);
