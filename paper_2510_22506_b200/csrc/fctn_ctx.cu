@@ -14,6 +14,7 @@
 #include <cstring>
 #include <map>
 #include <memory>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 #include <thread>
@@ -1277,6 +1278,8 @@ static thread_local std::string g_err;
 template <typename F>
 static int guarded(Ctx* c, F&& f) {
   try {
+    // every call runs on its context's device (several contexts / devices per process)
+    if (c && c->configured) CK(cudaSetDevice(c->device));
     f();
     return 0;
   } catch (const UsageError& e) {
@@ -1414,7 +1417,7 @@ struct Stager {
         const int b = (int)(c % NB);
         const size_t o = c * CH, m = std::min(CH, n - o);
         produce(o, m, b);
-        CK(cudaMemcpyAsync(buf[b], (const char*)src + (src_is_chunk ? 0 : o), m, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(buf[b], (const char*)src + o, m, cudaMemcpyDeviceToHost, st));
         CK(cudaEventRecord(ev[b], st));
       }
       if (c >= 1) {  // drain the previous chunk while this one moves
@@ -1426,14 +1429,52 @@ struct Stager {
       }
     }
   }
-  bool src_is_chunk = false;  // src is a per-chunk scratch (offset 0) rather than the whole tensor
 };
 
-static Stager& stager() {  // one ring per process (the library is not thread-safe per context)
-  static Stager* s = new Stager();
-  return *s;
+// One ring per device, leased under that device's mutex for a whole
+// transfer: contexts on different devices never share pinned buffers or
+// events (events belong to the device current at creation), and two threads
+// driving two contexts on one device take turns instead of sharing a slot.
+struct StagerLease {
+  std::unique_lock<std::mutex> lock;
+  Stager* s;
+  Stager* operator->() const { return s; }
+};
+static StagerLease stager() {
+  static std::mutex map_mu;
+  static std::map<int, std::pair<std::unique_ptr<std::mutex>, Stager*>> rings;
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  std::mutex* mu;
+  {
+    std::lock_guard<std::mutex> g(map_mu);
+    auto& slot = rings[dev];
+    if (!slot.first) {
+      slot.first.reset(new std::mutex());
+      slot.second = new Stager();  // created with `dev` current: its events live there
+    }
+    mu = slot.first.get();
+  }
+  StagerLease l{std::unique_lock<std::mutex>(*mu), nullptr};
+  std::lock_guard<std::mutex> g(map_mu);
+  l.s = rings[dev].second;
+  return l;
 }
-static bool use_stager(size_t bytes) { return bytes >= ((size_t)64 << 20) && !getenv("FCTN_NO_STAGE"); }
+// stream-ordered device scratch released on every exit path
+struct DevScratch {
+  void* p = nullptr;
+  cudaStream_t st;
+  DevScratch(size_t bytes, cudaStream_t s) : st(s) { CK(cudaMallocAsync(&p, bytes, st)); }
+  ~DevScratch() {
+    if (p) cudaFreeAsync(p, st);
+  }
+};
+static bool use_stager(size_t bytes) {
+  if (getenv("FCTN_NO_STAGE")) return false;
+  const char* m = getenv("FCTN_STAGE_MIN_BYTES");  // tests lower it to exercise the ring on small tensors
+  const size_t lo = m ? (size_t)std::strtoull(m, nullptr, 10) : ((size_t)64 << 20);
+  return bytes >= lo;
+}
 }  // namespace fctn
 
 extern "C" {
@@ -1445,21 +1486,20 @@ int fctn_upload_f64(fctn_ctx* c, const double* x_F, const uint8_t* mask_F) {
     const bool stage = fctn::use_stager((size_t)T * 8);
     fctn::HostPin pin_x(stage ? nullptr : x_F, stage ? 0 : (size_t)T * 8), pin_m(stage ? nullptr : mask_F, stage ? 0 : (size_t)T);
     if (x.dtype == FCTN_F64) {
-      if (stage) fctn::stager().h2d(x.X[0], x_F, (size_t)T * 8, x.st);
+      if (stage) fctn::stager()->h2d(x.X[0], x_F, (size_t)T * 8, x.st);
       else CK(cudaMemcpyAsync(x.X[0], x_F, T * 8, cudaMemcpyHostToDevice, x.st));
     } else {  // fp64 host data, fp32 context: convert on the device, in chunks
       const int64_t chunk = std::min<int64_t>(T, (int64_t)1 << 26);
-      double* tmp = nullptr;
-      CK(cudaMallocAsync((void**)&tmp, chunk * 8, x.st));
+      fctn::DevScratch scratch(chunk * 8, x.st);
+      double* tmp = (double*)scratch.p;
       for (int64_t o = 0; o < T; o += chunk) {
         const int64_t n = std::min(chunk, T - o);
-        if (stage) fctn::stager().h2d(tmp, x_F + o, (size_t)n * 8, x.st);
+        if (stage) fctn::stager()->h2d(tmp, x_F + o, (size_t)n * 8, x.st);
         else CK(cudaMemcpyAsync(tmp, x_F + o, n * 8, cudaMemcpyHostToDevice, x.st));
         fctn::launch_convert_f64_f32(tmp, (float*)x.X[0] + o, n, x.st);
       }
-      CK(cudaFreeAsync(tmp, x.st));
     }
-    if (stage) fctn::stager().h2d(x.mask, mask_F, (size_t)T, x.st);
+    if (stage) fctn::stager()->h2d(x.mask, mask_F, (size_t)T, x.st);
     else CK(cudaMemcpyAsync(x.mask, mask_F, T, cudaMemcpyHostToDevice, x.st));
     fctn::launch_pack_mask(x.mask, T, x.maskbits, x.st);
     CK(cudaStreamSynchronize(x.st));
@@ -1475,29 +1515,22 @@ int fctn_get_x_f64(fctn_ctx* c, double* x_F) {
     Ctx& x = c->impl;
     const int64_t T = x.sh.total();
     if (fctn::use_stager((size_t)T * 8)) {
-      fctn::Stager& sg = fctn::stager();
+      fctn::StagerLease lease = fctn::stager();
+      fctn::Stager& sg = *lease.s;
       if (x.dtype == FCTN_F64) {
-        sg.src_is_chunk = false;
         sg.d2h(x_F, x.X[x.cur], (size_t)T * 8, x.st, [](size_t, size_t, int) {});
       } else {  // convert each 32 MB chunk on the device into one of three scratch slots
-        double* tmp = nullptr;
         const size_t cd = fctn::Stager::CH / 8;  // doubles per chunk
-        CK(cudaMallocAsync((void**)&tmp, 3 * fctn::Stager::CH, x.st));
-        // the D2H of chunk c reads slot c % 3: issue it from that slot
-        sg.src_is_chunk = true;
-        int64_t chunk_id = 0;
+        fctn::DevScratch tmp(3 * fctn::Stager::CH, x.st);
         const float* X32 = (const float*)x.X[x.cur];
-        for (int64_t o = 0; o < T; o += (int64_t)cd, ++chunk_id) {
-          (void)o;
-        }
-        // explicit pipeline (the generic d2h reads one scratch address)
+        // explicit pipeline: chunk c is converted into scratch slot c % 3 and read from there
         const size_t n = (size_t)T * 8;
         const size_t nc = (n + fctn::Stager::CH - 1) / fctn::Stager::CH;
         for (size_t ci = 0; ci <= nc; ++ci) {
           if (ci < nc) {
             const int b = (int)(ci % fctn::Stager::NB);
             const size_t off = ci * fctn::Stager::CH, m = std::min(fctn::Stager::CH, n - off);
-            double* slot = tmp + (size_t)b * cd;
+            double* slot = (double*)tmp.p + (size_t)b * cd;
             fctn::launch_convert_f32_f64(X32 + off / 8, slot, (int64_t)(m / 8), x.st);
             CK(cudaMemcpyAsync(sg.buf[b], slot, m, cudaMemcpyDeviceToHost, x.st));
             CK(cudaEventRecord(sg.ev[b], x.st));
@@ -1510,8 +1543,6 @@ int fctn_get_x_f64(fctn_ctx* c, double* x_F) {
             sg.pcopy((char*)x_F + off, sg.buf[pb], m);
           }
         }
-        CK(cudaFreeAsync(tmp, x.st));
-        (void)chunk_id;
       }
       CK(cudaStreamSynchronize(x.st));
       return;
@@ -1915,7 +1946,7 @@ int fctn_quality(int device, int dtype, int n, const int64_t* dims, const void* 
     CK(cudaMallocAsync(&dt, T * es, st));
     if (mask_F) CK(cudaMallocAsync((void**)&dm, T, st));
     auto up = [&](void* d, const void* h, size_t n) {
-      if (fctn::use_stager(n)) fctn::stager().h2d(d, h, n, st);
+      if (fctn::use_stager(n)) fctn::stager()->h2d(d, h, n, st);
       else CK(cudaMemcpyAsync(d, h, n, cudaMemcpyHostToDevice, st));
     };
     up(de, est_F, T * es);
@@ -1941,7 +1972,7 @@ int fctn_quality_ctx(fctn_ctx* c, const void* truth_F, int truth_dtype, int mask
     const int64_t hw_global = x.gsh.dims[0] * x.gsh.dims[1];
     void* dt = nullptr;
     CK(cudaMallocAsync(&dt, T * es, x.st));
-    if (fctn::use_stager(T * es)) fctn::stager().h2d(dt, truth_F, T * es, x.st);
+    if (fctn::use_stager(T * es)) fctn::stager()->h2d(dt, truth_F, T * es, x.st);
     else CK(cudaMemcpyAsync(dt, truth_F, T * es, cudaMemcpyHostToDevice, x.st));
     fctn::quality_dispatch(x.dtype, truth_dtype, hw_local, hw_global, T / hw_local, x.n_sm, x.X[x.cur], dt,
                            mask_mode ? x.mask : nullptr, peak,

@@ -26,9 +26,11 @@ KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
 def launches(path):
     rows = [r for r in csv.reader(open(path)) if len(r) > 5]
     h = rows[0]
-    ki, vi = h.index("Kernel Name"), h.index("Metric Value")
+    ki, vi, mi = h.index("Kernel Name"), h.index("Metric Value"), h.index("Metric Name")
     agg = collections.defaultdict(lambda: [0, 0.0])
     for r in rows[1:]:
+        if r[mi] != "gpu__time_duration.sum":  # one row per (launch, metric): count time rows only
+            continue
         try:
             v = float(r[vi].replace(",", ""))
         except ValueError:
