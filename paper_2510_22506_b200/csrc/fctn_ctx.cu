@@ -441,9 +441,15 @@ class Ctx : public Executor {
       max_part = std::max(max_part, ((I + 63) / 64) * ((p + 63) / 64));
       max_ep = std::max(max_ep, (int64_t)fgram_splits(Ig) * S * S);
     }
-    if (n == 3)  // Y_1 partials of the Z route (split over b02)
+    if (n == 3) {  // Y_1 partials of the Z route (split over b02)
       max_yp = std::max(max_yp, sh.tri[sh.tri_index(0, 2)] * sh.dims[1] * sh.tri[sh.tri_index(0, 1)] *
                                     sh.tri[sh.tri_index(1, 2)]);
+      if (dtype == FCTN_F64) {  // the FP64 Z_0 pass stages its split partials here too (compute_z)
+        const int64_t I0 = sh.dims[0], p0 = T / I0, S0 = sh.s_of(0);
+        const StreamPlan sz = plan_stream(p0, S0, I0, target_ctas());
+        max_yp = std::max(max_yp, (int64_t)sz.nsplit * p0 * S0);
+      }
+    }
     A64.assign(n, nullptr);
     Ac.assign(n, nullptr);
     E64.assign(n, nullptr);
@@ -867,6 +873,7 @@ class Ctx : public Executor {
       }
     } else {
       StreamPlan sp = plan_stream(pj, Sj, Ij, target_ctas());
+      if ((int64_t)sp.nsplit * pj * Sj > ypart_cap) throw std::runtime_error("split-partial buffer too small (Z pass)");
       launch_stream<double>((const double*)X[cur], (const double*)fac_ptr(0), ypart, pj, Ij, Sj, Ij, sp, st);
       launch_reduce_splits(ypart, sp.nsplit, pj * Sj, nullptr, 0.0, (double*)Zb[0], st);
       ++launches;
@@ -933,6 +940,7 @@ class Ctx : public Executor {
     const bool tc = tc_ok(k);
     if (tc) {
       TcStreamPlan tp = plan_stream_tc(I, P, p / P, S, n_sm, split3);
+      if ((tp.nsplit * I * S + 1) / 2 > ypart_cap) throw std::runtime_error("split-partial buffer too small (stream)");
       const float* mh = (const float*)Mbuf;
       const float* ml = nullptr;
       if (split3 && S * p <= presplit_m_cap) {  // small M_k: split once in HBM, not per CTA in smem
@@ -946,6 +954,7 @@ class Ctx : public Executor {
       nsplit = (int)tp.nsplit;
     } else {
       StreamPlan sy = plan_stream(I, S, p, target_ctas());
+      if ((int64_t)sy.nsplit * I * S > ypart_cap) throw std::runtime_error("split-partial buffer too small (stream)");
       if (dtype == FCTN_F64)
         launch_stream<double>((const double*)X[cur], (const double*)Mbuf, ypart, I, P, S, p, sy, st);
       else

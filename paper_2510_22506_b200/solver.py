@@ -147,6 +147,8 @@ class SolverResult:
     initial_objective: float = math.nan
     # (iteration, metrics.QualityReport) when run(..., truth=...) is given
     quality: list = field(default_factory=list)
+    # iteration -> (x, factors) for run(..., snapshot_iters=...)
+    snapshots: dict = field(default_factory=dict)
 
     @property
     def iterations(self) -> int:
@@ -246,7 +248,7 @@ def _grow_with_continuity(dev: _Device, f: FctnFactors, cap: FctnRank, rng, scal
 
 
 def run(obs, cfg: SolverConfig, *, dtype: str = "float64", device: int | None = None, shard=None,
-        truth=None, peak: float = 1.0, quality_every: int = 0) -> SolverResult:
+        truth=None, peak: float = 1.0, quality_every: int = 0, snapshot_iters=()) -> SolverResult:
     """Same contract as `fctnlr.solver.run` (solver.py:277-399).
 
     ``truth`` (the full ground-truth tensor): `metrics.quality_report(x,
@@ -257,7 +259,11 @@ def run(obs, cfg: SolverConfig, *, dtype: str = "float64", device: int | None = 
     ``shard`` (a `shard.Shard`) runs this call as one rank of a mode-0 sharded
     sweep: every rank passes the same global observation and config; the
     returned ``x`` is this rank's slab (``result.slab`` = its rows of mode 0),
-    factors and trace are global and identical on every rank."""
+    factors and trace are global and identical on every rank.
+
+    ``snapshot_iters``: after each listed iteration X and the factors are
+    downloaded into ``result.snapshots[it] = (x, factors)`` (parity checks at
+    iterations 1, 5, ... from one run)."""
     if not isinstance(obs, Observation):
         obs = Observation(values=obs.values, mask=obs.mask)
     n = obs.values.ndim
@@ -340,6 +346,8 @@ def run(obs, cfg: SolverConfig, *, dtype: str = "float64", device: int | None = 
                 x_norm=math.sqrt(float(stats[_native.ST_XNEW_SQ])), factor_norm=factor_norm,
                 rank_grown=grown, device_ms=float(stats[_native.ST_DEVICE_MS])))
             stop = not grown and rel <= cfg.eps
+            if it in snapshot_iters:
+                result.snapshots[it] = (dev.ctx.get_x_f64(), dev.fetch_factors(rank, versions))
             if truth is not None and quality_every > 0 and it % quality_every == 0 and not (stop or it == cfg.max_iters):
                 result.quality.append((it, dev.quality(truth, peak)))
             if stop:

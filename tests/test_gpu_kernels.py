@@ -57,3 +57,26 @@ def test_chol_solves_match_numpy(S, H1):
         H = G + mu[w] * np.eye(S)
         np.testing.assert_allclose(H @ xr[w], Fr[w], rtol=1e-9, atol=1e-9 * np.abs(Fr[w]).max())
         np.testing.assert_allclose(H @ xi[w], Fi[w], rtol=1e-9, atol=1e-9 * np.abs(Fi[w]).max())
+
+
+@pytest.mark.parametrize("dtype", [_native.F64, _native.F32])
+def test_staged_transfers_roundtrip_partial_chunk(monkeypatch, dtype):
+    """The pinned staging ring (fctn_ctx.cu Stager) on a tensor of two 32 MB
+    chunks with a partial last one (threshold lowered by env), fp64 and the
+    fp32 device-side conversion; then a second context in the same process
+    (the ring is leased per device, not owned by the first context)."""
+    monkeypatch.setenv("FCTN_STAGE_MIN_BYTES", str(1 << 20))
+    dims = (1000, 700, 7)  # 4.9 M entries = 39.2 MB of fp64
+    rng = np.random.default_rng(11)
+    x = np.asfortranarray(rng.standard_normal(dims))
+    mask = np.asfortranarray(rng.random(dims) < 0.3)
+    want = x if dtype == _native.F64 else x.astype(np.float32).astype(np.float64)
+    for _ in range(2):
+        ctx = _native.Context(0, dtype, dims, (2, 2, 2), (0.35,) * 3, (0.5,) * 3, _native.SIGN_PD, 0.1,
+                              _native.ALG_ACCEL, 1 << 30)
+        try:
+            ctx.upload_f64(x, mask)
+            back = ctx.get_x_f64()
+        finally:
+            ctx.close()
+        assert np.array_equal(back, want)

@@ -25,8 +25,13 @@ def _cfg(d):
 @pytest.mark.parametrize("name", run_case_names())
 def test_gpu_matches_reference_golden(name):
     case = load_run(name)
-    res = P.run(P.Observation(case["values"], case["mask"]), _cfg(case["config"]))
+    res = P.run(P.Observation(case["values"], case["mask"]), _cfg(case["config"]), snapshot_iters=(1,))
     assert rel(res.x, case["x"]) <= FP64_TOL
+    # the reference's state after iteration 1 (its own max_iters=1 run)
+    x1, f1 = res.snapshots[1]
+    assert rel(x1, case["it1_x"]) <= FP64_TOL
+    for k, f in enumerate(case["it1_factors"]):
+        assert rel(f1.factor(k), f) <= FP64_TOL, k
     for k, f in enumerate(case["factors"]):
         assert res.factors.factor(k).shape == f.shape
         assert rel(res.factors.factor(k), f) <= FP64_TOL, k
@@ -40,6 +45,7 @@ def test_gpu_matches_reference_golden(name):
         assert r.iteration == i + 1
         assert r.objective == pytest.approx(case["trace_objective"][i], rel=FP64_TOL)
         assert r.x_norm == pytest.approx(case["trace_x_norm"][i], rel=1e-10)
+        assert r.rel_change == pytest.approx(case["trace_rel_change"][i], rel=1e-6, abs=1e-15)
         assert r.factor_norm == pytest.approx(case["trace_factor_norm"][i], rel=FP64_TOL)
         assert r.step_sq == pytest.approx(case["trace_step_sq"][i], rel=1e-6, abs=1e-12)
         assert (r.flops, r.mk_flops, r.compose_flops, r.cache_hits) == (
