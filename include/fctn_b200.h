@@ -155,6 +155,13 @@ int fctn_selftest_stream(int device, int dtype, int use_tc, int64_t I, int64_t P
  * [w + H1 s]), in place; `reps` timed launches, best ms returned. */
 int fctn_selftest_chol(int device, int64_t S, int64_t H1, const double* G, const double* mu, double* Fr, double* Fi,
                        int reps, double* ms_per_launch);
+/* Self-test of the eigendecomposition of the factor subproblem
+ * (sylvester.py:51-61 `eig_gram`): G (s x s, symmetric PSD, column-major)
+ * = V diag(phi) V^T.  V in: the warm-start basis (identity for a cold start),
+ * out: the eigenvectors; phi: eigenvalues clamped at 0; `sweeps`: Jacobi
+ * sweeps used; best ms over `reps` launches. */
+int fctn_selftest_eigh(int device, int64_t S, const double* G, double* V, double* phi, int reps, double* ms_per_launch,
+                       int* sweeps);
 
 /* Reconstruction quality (metrics.py:33-105).  The
  * first two modes are the image plane, every trailing-mode combination is a
@@ -208,6 +215,7 @@ int fctn_timer(fctn_ctx* ctx, int op, double* ms);
 #define FCTN_K_ZPASS 8    /* N=3 schedule: Z_0 = X x_0 A_(0) (tensor-core pass over X) */
 #define FCTN_K_YSMALL 9   /* N=3 schedule: Y_k = Z_0 (*) A_(l) (small contraction) */
 #define FCTN_K_MBUILD 10  /* M_k built outside the reference chain (compose operand) */
+#define FCTN_K_EIGH 11    /* K3 eigendecomposition of G_k (side stream, overlaps the Y_k pass) */
 #define FCTN_K_COUNT 12
 int fctn_set_profiling(fctn_ctx* ctx, int on);
 int fctn_get_profile(fctn_ctx* ctx, double* ms, int64_t* launches, double* bytes);

@@ -24,12 +24,12 @@ CT_FLOPS, CT_MK, CT_COMPOSE, CT_HITS, CT_LAUNCHES, CT_COUNT = 0, 1, 2, 3, 4, 8
 EXPORTS = [
     "fctn_create", "fctn_upload", "fctn_upload_f64", "fctn_get_x_f64", "fctn_set_factors", "fctn_set_rank", "fctn_get_factors", "fctn_get_x",
     "fctn_objective", "fctn_sweep", "fctn_plan_sweeps", "fctn_nccl_unique_id", "fctn_set_comm", "fctn_set_comm_host",
-    "fctn_sync", "fctn_selftest_stream", "fctn_selftest_chol", "fctn_timer", "fctn_set_profiling", "fctn_get_profile", "fctn_last_error", "fctn_version",
+    "fctn_sync", "fctn_selftest_stream", "fctn_selftest_chol", "fctn_selftest_eigh", "fctn_timer", "fctn_set_profiling", "fctn_get_profile", "fctn_last_error", "fctn_version",
     "fctn_quality", "fctn_quality_ctx", "fctn_destroy",
 ]
 Q_PSNR, Q_SSIM, Q_ERR_SQ, Q_REF_SQ, Q_OFF_ERR_SQ, Q_OFF_REF_SQ, Q_OFF_COUNT, Q_COUNT = 0, 1, 2, 3, 4, 5, 6, 8
 K_CLASSES = ["merge", "stream_y", "gram", "reduce", "chol", "compose", "dft", "fgram", "zpass", "ysmall", "mbuild",
-             "k11"]
+             "eigh"]
 
 _lib = None
 
@@ -98,6 +98,7 @@ def lib():
     L.fctn_set_comm_host.argtypes = [P, HOST_ALLREDUCE, HOST_ALLGATHER, P, C.c_int, C.c_int, C.c_int64, C.c_int64]
     L.fctn_sync.argtypes = [P]
     L.fctn_selftest_chol.argtypes = [C.c_int, C.c_int64, C.c_int64, P, P, P, P, C.c_int, f64p]
+    L.fctn_selftest_eigh.argtypes = [C.c_int, C.c_int64, P, P, P, C.c_int, f64p, C.POINTER(C.c_int)]
     L.fctn_selftest_stream.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int64, C.c_int64, C.c_int64, C.c_int64, P, P,
                                        f64p]
     L.fctn_timer.argtypes = [P, C.c_int, f64p]
@@ -205,6 +206,21 @@ def selftest_chol(G, mu, Fr, Fi, reps=1, device=0):
                                   C.byref(ms))
     check(rc)
     return fr, fi, float(ms.value)
+
+
+def selftest_eigh(G, V0=None, reps=1, device=0):
+    """G = V diag(phi) V^T on the device (eigh.cu); returns (V, phi, best ms,
+    Jacobi sweeps).  V0: warm-start basis (identity by default)."""
+    G = np.asfortranarray(G, dtype=np.float64)
+    S = G.shape[0]
+    V = np.asfortranarray(np.eye(S) if V0 is None else V0, dtype=np.float64).copy(order="F")
+    phi = np.zeros(S)
+    ms = C.c_double()
+    sw = C.c_int()
+    rc = lib().fctn_selftest_eigh(int(device), S, G.ctypes.data_as(C.c_void_p), V.ctypes.data_as(C.c_void_p),
+                                  phi.ctypes.data_as(C.c_void_p), int(reps), C.byref(ms), C.byref(sw))
+    check(rc)
+    return V, phi, float(ms.value), int(sw.value)
 
 
 class Context:

@@ -122,6 +122,35 @@ class Ctx : public Executor {
   std::vector<DftPlan> dft;
   std::vector<double*> mu, cosT, sinT;
   std::vector<double> check_mu;
+  // eigenbasis solve (eigh.cu): per-mode basis V_k (warm start across sweeps),
+  // eigenvalues, the T-floor shift lam min(Lambda) + rho, a rotation scratch,
+  // and the side stream the Gram network + eigendecomposition run on
+  std::vector<double*> Vb;
+  std::vector<double> floor_shift;
+  double* phi = nullptr;
+  double* Ytmp = nullptr;
+  double* ework = nullptr;
+  double* dft_gscr = nullptr;  // column work arrays of long-mode DFTs (I > 4266)
+  cudaStream_t st2 = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  int solve_pref = 0;  // FCTN_SOLVE: 0 auto, 1 = "chol", 2 = "eigh"
+  // Which form solves update k.  The eigenbasis form (eigh.cu, the
+  // reference's own) runs on a side stream concurrently with the Y_k pass, so
+  // it is off the critical path when its single-SM Jacobi is shorter than
+  // that pass.  s > 160 has no Cholesky kernel: always eigh (from global
+  // memory above s = 117).  The choice depends only on global shapes and the
+  // visiting order, so every rank of a sharded run makes the same one.
+  bool eigh_for(int k, bool long_y) const {
+    const int64_t S = gsh.s_of(k);
+    if (S > 160) return true;
+    if (solve_pref == 1 || !eigh_fits_smem(S)) return false;
+    if (solve_pref == 2) return true;
+    // auto: measured on B200 the single-SM Jacobi (c4 s = 64: ~0.6 ms warm,
+    // c5 s = 81: ~1.2 ms) exceeds the Y_k passes it would hide under, while
+    // the all-SM Cholesky takes 0.08 ms; keep the Cholesky form
+    (void)long_y;
+    return false;
+  }
   double* dstats = nullptr;  // [n*3 factor stats][4 sums]
   int* dstatus = nullptr;
   double* hstats = nullptr;  // pinned mirror (+ status)
@@ -159,6 +188,7 @@ class Ctx : public Executor {
     cudaEvent_t a, b;
     double bytes;
     int64_t n;
+    cudaStream_t s;
   };
   bool prof = false;
   int prof_cls = FCTN_K_MERGE;  // class of generic contractions (merge unless set)
@@ -179,10 +209,10 @@ class Ctx : public Executor {
     CK(cudaEventCreate(&e));
     return e;
   }
-  int pbegin(int cls) {
+  int pbegin(int cls, cudaStream_t on = nullptr) {
     if (!prof) return -1;
-    Mark m{cls, take_event(), take_event(), 0.0, 0};
-    CK(cudaEventRecord(m.a, st));
+    Mark m{cls, take_event(), take_event(), 0.0, 0, on ? on : st};
+    CK(cudaEventRecord(m.a, m.s));
     marks.push_back(m);
     return (int)marks.size() - 1;
   }
@@ -191,7 +221,7 @@ class Ctx : public Executor {
     Mark& m = marks[idx];
     m.bytes = bytes;
     m.n = n;
-    CK(cudaEventRecord(m.b, st));
+    CK(cudaEventRecord(m.b, m.s));
   }
   void collect_marks() {  // after a stream sync
     for (auto& m : marks) {
@@ -367,6 +397,10 @@ class Ctx : public Executor {
     presplit_m_cap = 0;
     for (auto* p : E64) cudaFree(p);
     E64.clear();
+    for (auto* p : Vb) cudaFree(p);
+    Vb.clear();
+    for (auto* p : {phi, Ytmp, ework, dft_gscr}) cudaFree(p);
+    phi = Ytmp = ework = dft_gscr = nullptr;
     Ascratch = nullptr;
     Mbuf = nullptr;
     Y = G = Fr = Fi = ypart = partials = epart = colstats = gnet[0] = gnet[1] = nullptr;
@@ -398,6 +432,11 @@ class Ctx : public Executor {
     hstats = nullptr;
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_join) cudaEventDestroy(ev_join);
+    ev_fork = ev_join = nullptr;
+    if (st2) cudaStreamDestroy(st2);
+    st2 = nullptr;
     if (st) cudaStreamDestroy(st);
     ev0 = ev1 = nullptr;
     st = nullptr;
@@ -485,6 +524,21 @@ class Ctx : public Executor {
     z_invalidate();
     mbuf_holds = -1;
     CK(cudaMalloc(&Y, max_is * sizeof(double)));
+    CK(cudaMalloc(&Ytmp, max_is * sizeof(double)));
+    CK(cudaMalloc(&phi, max_s * sizeof(double)));
+    Vb.assign(n, nullptr);
+    for (int k = 0; k < n; ++k) {
+      const int64_t S = gsh.s_of(k);
+      CK(cudaMalloc(&Vb[k], S * S * sizeof(double)));
+      launch_identity(Vb[k], S, st);  // the first eigendecomposition starts cold
+    }
+    {
+      int64_t gs = 0;
+      for (int k = 0; k < n; ++k)
+        if (!dft[k].fast) gs = std::max(gs, 6 * gsh.dims[k] * gsh.s_of(k));
+      if (gs) CK(cudaMalloc(&dft_gscr, gs * sizeof(double)));
+    }
+    if (!eigh_fits_smem(max_s)) CK(cudaMalloc(&ework, (2 * max_s * max_s + max_s) * sizeof(double)));
     CK(cudaMalloc(&G, max_ss * sizeof(double)));
     CK(cudaMalloc(&Fr, max_h * sizeof(double)));
     CK(cudaMalloc(&Fi, max_h * sizeof(double)));
@@ -609,13 +663,13 @@ class Ctx : public Executor {
     }
     return peak;
   }
-  void gram_network(int k) {
+  void gram_network(int k, cudaStream_t gs) {
     std::vector<int> rest;
     for (int j = 0; j < sh.n; ++j)
       if (j != k) rest.push_back(j);
     const int64_t S = sh.s_of(k);
     if (rest.size() == 1) {  // n == 2: G_k = E_j
-      CK(cudaMemcpyAsync(G, E64[rest[0]], S * S * sizeof(double), cudaMemcpyDeviceToDevice, st));
+      CK(cudaMemcpyAsync(G, E64[rest[0]], S * S * sizeof(double), cudaMemcpyDeviceToDevice, gs));
       return;
     }
     LTensor cur;
@@ -633,7 +687,7 @@ class Ctx : public Executor {
       ContractDesc d = desc_for(op, &sw);
       const double* pa = cur_ptr;
       const double* pb = E64[rest[q]];
-      launch_contract<double>(sw ? pb : pa, sw ? pa : pb, out_ptr, d, cscratch, cscratch_cap, n_sm, st);
+      launch_contract<double>(sw ? pb : pa, sw ? pa : pb, out_ptr, d, cscratch, cscratch_cap, n_sm, gs);
       ++launches;
       cur = op.out;
       cur_ptr = out_ptr;
@@ -693,8 +747,16 @@ class Ctx : public Executor {
       split3 = !(t && std::string(t) == "1x");
     }
     CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&st2, cudaStreamNonBlocking));
     CK(cudaEventCreate(&ev0));
     CK(cudaEventCreate(&ev1));
+    CK(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
+    {
+      const char* sv = getenv("FCTN_SOLVE");
+      const std::string v = sv ? sv : "";
+      solve_pref = v == "chol" ? 1 : v == "eigh" ? 2 : 0;
+    }
     {
       cudaMemPool_t pool;
       CK(cudaDeviceGetDefaultMemPool(&pool, device));
@@ -716,11 +778,11 @@ class Ctx : public Executor {
     cosT.assign(n, nullptr);
     sinT.assign(n, nullptr);
     check_mu.assign(n, NAN);
+    floor_shift.assign(n, 0.0);
     dft.clear();
     for (int k = 0; k < n; ++k) {
       int64_t I = sh.dims[k];
       dft.push_back(plan_dft(I));
-      if (!dft.back().fast) throw UsageError("mode extent " + std::to_string(I) + " exceeds the on-chip DFT limit");
       std::vector<double> c(I), s(I), m(I / 2 + 1);
       double lmin = INFINITY;
       for (int64_t j = 0; j < I; ++j) {
@@ -733,6 +795,7 @@ class Ctx : public Executor {
       }
       // T-floor guard (sylvester.py:108-113): min T = lam*min(Lambda) + phi_min + rho.
       // It can only fail when lam*min(Lambda) + rho <= 1e-10 (phi >= 0 after the clamp).
+      floor_shift[k] = lam[k] * lmin + rho;
       double shift = lam[k] * lmin + rho - 1e-10;
       if (shift <= 0.0) check_mu[k] = shift;
       CK(cudaMalloc(&mu[k], m.size() * sizeof(double)));
@@ -920,13 +983,31 @@ class Ctx : public Executor {
   }
 
   void factor_update(int k, int zj, int extrap, double alpha, double beta) {
+    const bool long_y = zj < 0 || zver[zj] != planner->versions[zj];
+    const bool eg = eigh_for(k, long_y);
+    if (eg) {
+      // G_k and its eigendecomposition need only the other factors' Grams:
+      // run them on the side stream while this stream forms Y_k
+      CK(cudaEventRecord(ev_fork, st));
+      CK(cudaStreamWaitEvent(st2, ev_fork, 0));
+      const int64_t S = gsh.s_of(k);
+      int pm = pbegin(FCTN_K_GRAM, st2);
+      int64_t l0 = launches;
+      gram_network(k, st2);
+      pend(pm, 8.0 * S * S, launches - l0);
+      pm = pbegin(FCTN_K_EIGH, st2);
+      launch_eigh(G, S, Vb[k], phi, ework, floor_shift[k], dstatus, 40, st2);
+      ++launches;
+      pend(pm, 8.0 * 3 * S * S, 1);
+      CK(cudaEventRecord(ev_join, st2));
+    }
     if (zj >= 0) {
       if (zver[zj] != planner->versions[zj]) compute_z(zj);
       y_from_z(zj, k);
     } else {
       y_stream(k);
     }
-    solve_factor(k, extrap, alpha, beta);
+    solve_factor(k, eg, extrap, alpha, beta);
   }
 
   void y_stream(int k) {
@@ -975,21 +1056,39 @@ class Ctx : public Executor {
     if (sharded()) finish_y(k, k == 0);
   }
 
-  void solve_factor(int k, int extrap, double alpha, double beta) {
+  void solve_factor(int k, bool eg, int extrap, double alpha, double beta) {
     const int64_t T = gsh.total();
     const int64_t I = gsh.dims[k], S = gsh.s_of(k), p = T / I;
-    // G_k = M_k M_k^T by the doubled network (sylvester.py:57-59)
-    int pm = pbegin(FCTN_K_GRAM);
-    int64_t l0 = launches;
-    gram_network(k);
-    pend(pm, 8.0 * S * S, launches - l0);
     planner->meter.proj += 2 * I * p * S;   // sylvester.py:105
     planner->meter.gram += 2 * S * S * p;   // sylvester.py:58
-    // K3: DFT along mode k, per-frequency SPD solves, inverse DFT (sylvester.py:108-116)
     const DftPlan& dp = dft[k];
     const double sgn = sign == FCTN_SIGN_PD ? -1.0 : 1.0;
+    int pm;
+    if (eg) {
+      // the reference's closed form (sylvester.py:108-116) in the basis from
+      // the side stream: A = Re(F^H [(F (Y V)) / T]) V^T
+      CK(cudaStreamWaitEvent(st, ev_join, 0));
+      pm = pbegin(FCTN_K_DFT);
+      launch_rotate<double>(Y, I, S, Vb[k], false, Ytmp, nullptr, 0, 0.0, 0.0, (double*)nullptr, st);
+      launch_dft_fwd(Ytmp, dp, S, cosT[k], sinT[k], Fr, Fi, st, dft_gscr);
+      launch_dft_inv<double>(Fr, Fi, dp, S, cosT[k], sinT[k], nullptr, Ytmp, (double*)nullptr, 0, 0.0, 0.0,
+                             delta[k], sgn, nullptr, st, mu[k], phi, dft_gscr);
+      if (dtype == FCTN_F64)
+        launch_rotate<double>(Ytmp, I, S, Vb[k], true, Ascratch, A64[k], extrap, alpha, beta, (double*)nullptr, st);
+      else
+        launch_rotate<float>(Ytmp, I, S, Vb[k], true, Ascratch, A64[k], extrap, alpha, beta, (float*)Ac[k], st);
+      launch_colstats3(Ascratch, A64[k], I, S, delta[k], sgn, colstats, st);
+      launches += 5;
+      pend(pm, 8.0 * (6.0 * I * S + 4.0 * dp.H1 * S), 5);
+    } else {
+    // G_k = M_k M_k^T by the doubled network (sylvester.py:57-59)
+    pm = pbegin(FCTN_K_GRAM);
+    int64_t l0 = launches;
+    gram_network(k, st);
+    pend(pm, 8.0 * S * S, launches - l0);
+    // K3: DFT along mode k, per-frequency SPD solves, inverse DFT (sylvester.py:108-116)
     pm = pbegin(FCTN_K_DFT);
-    launch_dft_fwd(Y, dp, S, cosT[k], sinT[k], Fr, Fi, st);
+    launch_dft_fwd(Y, dp, S, cosT[k], sinT[k], Fr, Fi, st, dft_gscr);
     pend(pm, 8.0 * (I * S + 2.0 * dp.H1 * S), 1);
     pm = pbegin(FCTN_K_SOLVE);
     launch_chol_solve(G, S, dp.H1, mu[k], Fr, Fi, check_mu[k], dstatus, st);
@@ -997,11 +1096,14 @@ class Ctx : public Executor {
     pm = pbegin(FCTN_K_DFT);
     const int ninv = dtype == FCTN_F64
                          ? launch_dft_inv<double>(Fr, Fi, dp, S, cosT[k], sinT[k], A64[k], Ascratch, nullptr, extrap,
-                                                  alpha, beta, delta[k], sgn, colstats, st)
+                                                  alpha, beta, delta[k], sgn, colstats, st, nullptr, nullptr,
+                                                  dft_gscr)
                          : launch_dft_inv<float>(Fr, Fi, dp, S, cosT[k], sinT[k], A64[k], Ascratch, (float*)Ac[k],
-                                                 extrap, alpha, beta, delta[k], sgn, colstats, st);
+                                                 extrap, alpha, beta, delta[k], sgn, colstats, st, nullptr, nullptr,
+                                                 dft_gscr);
     launches += ninv - 1;
     pend(pm, 8.0 * (3.0 * I * S + 2.0 * dp.H1 * S), ninv);
+    }
     pm = pbegin(FCTN_K_FGRAM);
     launch_factor_gram(Ascratch, I, S, epart, E64[k], colstats, dstats + 3 * k, st);
     pend(pm, 8.0 * (I * S + S * S), 2);
@@ -1078,6 +1180,9 @@ class Ctx : public Executor {
   void sweep_device(const std::vector<int>& order, int extrap, double alpha, double beta) {
     const int n = sh.n;
     const std::vector<int> route = plan_routes(order);
+    bool side = false;
+    for (int k = 0; k < n; ++k) side |= eigh_for(k, true);
+    tc_reserve_sms(side ? 1 : 0);  // one SM for the concurrent eigendecomposition
     for (size_t t = 0; t < order.size(); ++t) {
       const int k = order[t];
       const bool zr = route[t] >= 0;
@@ -1823,6 +1928,49 @@ int fctn_selftest_stream(int device, int dtype, int use_tc, int64_t I, int64_t P
     cudaFree(dm);
     cudaFree(dy);
     cudaFree(part);
+    cudaStreamDestroy(st);
+  });
+}
+
+int fctn_selftest_eigh(int device, int64_t S, const double* G, double* V, double* phi, int reps,
+                       double* ms_per_launch, int* sweeps) {
+  return fctn::guarded(nullptr, [&] {
+    CK(cudaSetDevice(device));
+    cudaStream_t st;
+    CK(cudaStreamCreate(&st));
+    double *dG, *dV0, *dV, *dphi, *work = nullptr;
+    int *dstat, *dsw;
+    CK(cudaMalloc(&dG, S * S * 8));
+    CK(cudaMalloc(&dV0, S * S * 8));
+    CK(cudaMalloc(&dV, S * S * 8));
+    CK(cudaMalloc(&dphi, S * 8));
+    CK(cudaMalloc(&dstat, 4));
+    CK(cudaMalloc(&dsw, 4));
+    if (!fctn::eigh_fits_smem(S)) CK(cudaMalloc(&work, (2 * S * S + S) * 8));
+    CK(cudaMemset(dstat, 0, 4));
+    CK(cudaMemcpy(dG, G, S * S * 8, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(dV0, V, S * S * 8, cudaMemcpyHostToDevice));
+    cudaEvent_t a, b;
+    CK(cudaEventCreate(&a));
+    CK(cudaEventCreate(&b));
+    float best = 1e30f;
+    for (int r = 0; r < std::max(reps, 1); ++r) {
+      CK(cudaMemcpyAsync(dV, dV0, S * S * 8, cudaMemcpyDeviceToDevice, st));
+      CK(cudaEventRecord(a, st));
+      fctn::launch_eigh(dG, S, dV, dphi, work, 1.0, dstat, 40, st, dsw);
+      CK(cudaEventRecord(b, st));
+      CK(cudaEventSynchronize(b));
+      float ms = 0.f;
+      CK(cudaEventElapsedTime(&ms, a, b));
+      best = std::min(best, ms);
+    }
+    CK(cudaMemcpy(V, dV, S * S * 8, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(phi, dphi, S * 8, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(sweeps, dsw, 4, cudaMemcpyDeviceToHost));
+    *ms_per_launch = best;
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    for (void* p : {(void*)dG, (void*)dV0, (void*)dV, (void*)dphi, (void*)dstat, (void*)dsw, (void*)work}) cudaFree(p);
     cudaStreamDestroy(st);
   });
 }

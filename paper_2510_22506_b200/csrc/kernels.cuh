@@ -105,6 +105,8 @@ TcStreamPlan plan_stream_tc(int64_t I, int64_t P, int64_t Q, int64_t S, int n_sm
 void launch_stream_tc(const float* X, const float* M, float* part, int64_t I, int64_t P, int64_t Q, int64_t S,
                       const TcStreamPlan& tp, cudaStream_t st, const float* Mlo = nullptr);
 bool tc_stream_batched_supported(int64_t R, int64_t Q, int64_t NB, int64_t S);
+// persistent tensor-core passes leave n SMs free (side-stream work)
+void tc_reserve_sms(int n);
 void launch_stream_tc_batched(const float* X, const float* Bh, const float* Bl, float* out, int64_t R, int64_t Q,
                               int64_t NB, int64_t S, int n_sm, cudaStream_t st);
 
@@ -116,8 +118,9 @@ struct DftPlan {
 };
 DftPlan plan_dft(int64_t I);
 // F[w + H1*s] = sum_j Y[j + I*s] exp(-2 pi i w j / I), w < H1  (laplacian.py:75-81)
+// (modes with p.fast == false run from `gscr`: 6 I doubles per column)
 void launch_dft_fwd(const double* Y, const DftPlan& p, int64_t S, const double* cosT, const double* sinT,
-                    double* Fr, double* Fi, cudaStream_t st);
+                    double* Fr, double* Fi, cudaStream_t st, double* gscr = nullptr);
 // per-frequency Cholesky solves of (G + mu_w I) a_w = F_w; extra check CTA
 // when check_mu is finite (T-floor test, sylvester.py:108-113)
 void launch_chol_solve(const double* G, int64_t S, int64_t H1, const double* mu, double* Fr, double* Fi,
@@ -127,7 +130,24 @@ void launch_chol_solve(const double* G, int64_t S, int64_t H1, const double* mu,
 template <typename T>
 int launch_dft_inv(const double* Fr, const double* Fi, const DftPlan& p, int64_t S, const double* cosT,
                     const double* sinT, const double* Aold, double* Anew, T* Acompute, int extrap, double alpha,
-                    double beta, double delta, double sgn, double* colstats, cudaStream_t st);
+                    double beta, double delta, double sgn, double* colstats, cudaStream_t st,
+                    const double* mu = nullptr, const double* phi = nullptr, double* gscr = nullptr);
+// eigenbasis form of the solve (eigh.cu; sylvester.py:51-61,98-116):
+// G = V diag(phi) V^T by one-sided Jacobi (V in: warm start, out: basis);
+// status |= 1 when floor_shift + min(phi) <= 1e-10 (T floor), 2 if non-finite
+size_t eigh_smem_bytes(int64_t S);
+bool eigh_fits_smem(int64_t S);
+void launch_eigh(const double* G, int64_t S, double* V, double* phi, double* work, double floor_shift, int* status,
+                 int max_sweeps, cudaStream_t st, int* nsweeps = nullptr);
+// out = A W, W = V or V^T (A: I x S); with aold: extrapolation epilogue and the
+// compute-dtype copy acomp
+template <typename T>
+void launch_rotate(const double* A, int64_t I, int64_t S, const double* V, bool trans, double* out,
+                   const double* aold, int extrap, double alpha, double beta, T* acomp, cudaStream_t st);
+void launch_identity(double* V, int64_t S, cudaStream_t st);
+// [||a - a_old||^2, ||a||^2, a.(L a)] per column
+void launch_colstats3(const double* A, const double* Aold, int64_t I, int64_t S, double delta, double sgn,
+                      double* colstats, cudaStream_t st);
 // per-column [0, ||a||^2, a.(L a)] without a previous iterate
 void launch_factor_colstats(const double* A, int64_t I, int64_t S, double delta, double sgn, double* colstats,
                             cudaStream_t st);

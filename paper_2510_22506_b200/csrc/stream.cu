@@ -43,7 +43,7 @@ StreamPlan plan_stream(int64_t I, int64_t S, int64_t p, int target_ctas) {
   return sp;
 }
 
-// CTA: TI (= NTI*RI) rows of mode k x TS bond columns, one p-chunk.
+// CTA: TI (= NTI*RI) rows of mode k x TS bond columns (column tile z), one p-chunk.
 template <typename T, int TS, int RI, bool XFAST>
 __global__ void __launch_bounds__(256) k_stream(const T* __restrict__ X, const T* __restrict__ M,
                                                 double* __restrict__ part, int64_t I, int64_t P, int64_t S,
@@ -59,6 +59,7 @@ __global__ void __launch_bounds__(256) k_stream(const T* __restrict__ X, const T
   const int64_t i0 = (int64_t)blockIdx.x * TI;
   const int64_t split = blockIdx.y;
   const int64_t pb = split * chunk;
+  const int64_t s0 = (int64_t)blockIdx.z * TS;  // column tile (s > TS)
   int64_t pe = pb + chunk;
   if (pe > p) pe = p;
   const int64_t PI = P * I;
@@ -85,7 +86,7 @@ __global__ void __launch_bounds__(256) k_stream(const T* __restrict__ X, const T
     for (int e = tid; e < PC * TS; e += 256) {
       const int pp = e % PC, s = e / PC;
       const int64_t gp = p0 + pp;
-      Ms[pp][s] = (gp < pe && s < S) ? M[gp + p * s] : T(0);
+      Ms[pp][s] = (gp < pe && s0 + s < S) ? M[gp + p * (s0 + s)] : T(0);
     }
     __syncthreads();
 #pragma unroll 4
@@ -109,7 +110,7 @@ __global__ void __launch_bounds__(256) k_stream(const T* __restrict__ X, const T
     if (gi >= I) continue;
 #pragma unroll
     for (int b = 0; b < 4; ++b) {
-      const int64_t s = ts + NTS * b;
+      const int64_t s = s0 + ts + NTS * b;
       if (s < S) out[gi + I * s] = (double)acc[a][b];
     }
   }
@@ -118,7 +119,7 @@ __global__ void __launch_bounds__(256) k_stream(const T* __restrict__ X, const T
 template <typename T, int TS, int RI>
 static void stream_go(const T* X, const T* M, double* part, int64_t I, int64_t P, int64_t S, int64_t p,
                       const StreamPlan& sp, cudaStream_t st) {
-  dim3 grid(sp.n_itiles, sp.nsplit);
+  dim3 grid(sp.n_itiles, sp.nsplit, (unsigned)((S + TS - 1) / TS));
   if (P == 1)
     k_stream<T, TS, RI, true><<<grid, 256, 0, st>>>(X, M, part, I, P, S, p, sp.chunk);
   else

@@ -801,6 +801,10 @@ int sm_count() {
   return v;
 }
 
+// SMs kept free of the persistent kernels (the context reserves one while the
+// side-stream eigendecomposition runs concurrently, eigh.cu)
+int g_reserved_sms = 0;
+
 template <int NT, bool AMN>
 void go_ts(const CUtensorMap& mx, const CUtensorMap& mm, const CUtensorMap& mml, bool b_pre, bool x3d, float* part,
            int64_t I, int64_t S, const TcStreamPlan& tp, cudaStream_t st, int rows_b = 0) {
@@ -811,7 +815,7 @@ void go_ts(const CUtensorMap& mx, const CUtensorMap& mm, const CUtensorMap& mml,
       auto fn = k_stream_tsp<NT, AMN>;
       cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
       if (e != cudaSuccess) throw std::runtime_error(std::string("stream_tsp smem: ") + cudaGetErrorString(e));
-      const int grid = (int)std::min<int64_t>(tp.n_mtiles, sm_count());
+      const int grid = (int)std::min<int64_t>(tp.n_mtiles, std::max(1, sm_count() - g_reserved_sms));
       fn<<<grid, TSP_THREADS, smem, st>>>(mx, mm, mml, part, (int)I, (int)S, (int)tp.nkb, (int)tp.n_mtiles,
                                           (int)tp.npb, b_pre ? 1 : 0, x3d ? 1 : 0, rows_b);
       e = cudaGetLastError();
@@ -850,6 +854,8 @@ void go(const CUtensorMap& mx, const CUtensorMap& mx3, const CUtensorMap& mm, co
 }
 
 }  // namespace
+
+void tc_reserve_sms(int n) { g_reserved_sms = n; }
 
 CUtensorMap tc_make_map_f32(const void* base, int rank, const uint64_t* dims, const uint64_t* strides_bytes,
                             const uint32_t* box, bool mn32) {

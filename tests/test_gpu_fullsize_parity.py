@@ -29,8 +29,11 @@ from tests.golden_util import GOLDEN, rel
 pytestmark = pytest.mark.gpu
 FP64_TOL = 1e-9
 DIFF_TOL = 1e-6       # step_sq / rel_change (cancellation-amplified)
-FP32_X_TOL = 1e-3     # relative, sampled X and objective trace (3xTF32 products, 20 sweeps)
-FP32_F_TOL = 1e-2     # relative, per factor (gauge directions amplify product rounding)
+# measured on B200 (profiles/r02/fullsize_parity.json): X 1.1e-4 (c4) / 1.9e-4
+# (c5), factors 1.4e-3 / 4.5e-4, objective 6.2e-4 / 1.9e-6, dPSNR 3.5e-3 /
+# 1.1e-5 dB
+FP32_X_TOL = 1e-3     # relative, sampled X, slice sums and objective trace (3xTF32 products, 20 sweeps)
+FP32_F_TOL = 5e-3     # relative, per factor (gauge directions amplify product rounding)
 FP32_PSNR_DB = 0.01   # north_star
 OUT = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "gpurun_out")
 

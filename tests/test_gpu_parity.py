@@ -197,3 +197,43 @@ def test_gpu_split_dft_fp64(dims, rank):
     for a, b in zip(res.trace, ref.trace):
         assert a.objective == pytest.approx(b.objective, rel=FP64_TOL)
         assert a.step_sq == pytest.approx(b.step_sq, rel=1e-6, abs=1e-12)
+
+
+@pytest.mark.parametrize("solve", ["eigh", "chol"])
+@pytest.mark.parametrize("name", ["n3_afctnlr", "n4_afctnlr_shuffle", "n5_budget_binds", "n3_extrapolation",
+                                  "n4_nonuniform_rank", "c3_scaled"])
+def test_gpu_solve_forms_match_reference_golden(monkeypatch, name, solve):
+    """Both device forms of the factor subproblem against the reference:
+    the eigenbasis form (eigh.cu, the reference's own sylvester.py:51-61,
+    98-116) and the per-frequency Cholesky form, forced for every update."""
+    monkeypatch.setenv("FCTN_SOLVE", solve)
+    case = load_run(name)
+    res = P.run(P.Observation(case["values"], case["mask"]), _cfg(case["config"]))
+    assert rel(res.x, case["x"]) <= FP64_TOL
+    for k, f in enumerate(case["factors"]):
+        assert rel(res.factors.factor(k), f) <= FP64_TOL, k
+    for i, r in enumerate(res.trace):
+        assert r.objective == pytest.approx(case["trace_objective"][i], rel=FP64_TOL)
+
+
+@pytest.mark.parametrize("dims,rank,iters", [
+    ((8192, 6, 5), 2, 6),       # I_0 = 8192 > 4266: the long-mode DFT from global scratch
+    ((5000, 7, 3), 3, 4),       # long mode with a non-power-of-two extent
+    ((8, 7, 6, 5), 6, 4),       # N = 4, R = 6: s = 216 > 160, the global-memory Jacobi solve
+])
+def test_gpu_general_sizes_match_oracle(dims, rank, iters):
+    """Inputs beyond the on-chip limits the reference also accepts
+    (laplacian.py:75-81 np.fft, sylvester.py:60 eigh): FP64 parity with the
+    oracle at the north_star bound."""
+    rng = np.random.default_rng(sum(dims))
+    truth = rng.standard_normal(dims)
+    mask = rng.random(dims) < 0.5
+    kw = dict(lam=0.35, delta=0.5, rho=0.1, eps=0.0, max_iters=iters, max_rank=rank, initial_rank=rank,
+              rank_policy="fixed", algorithm="afctnlr", shuffle=True, seed=0)
+    ref = O.run(truth, mask, **kw)
+    res = P.run(P.Observation(truth, mask), P.SolverConfig(**kw))
+    assert rel(res.x, ref.x) <= FP64_TOL
+    for k in range(len(dims)):
+        assert rel(res.factors.factor(k), ref.factors[k]) <= FP64_TOL, k
+    for a, b in zip(res.trace, ref.trace):
+        assert a.objective == pytest.approx(b.objective, rel=FP64_TOL)
