@@ -47,6 +47,27 @@ def peaks():
     return dict(PEAKS_FALLBACK)
 
 
+def compute_peaks():
+    """FP64 / FP32 / TF32 GEMM peaks measured on a B200 of this pool by
+    tools/measure_peaks.py (committed under profiles/)."""
+    p = os.path.join(ROOT, "profiles", "compute_peaks.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        d["source"] = "measured (profiles/compute_peaks.json, tools/measure_peaks.py)"
+        return d
+    return {"fp64_tflops": 37.0, "tf32_tensor_tflops": 1100.0, "fp32_simt_tflops": 75.0,
+            "source": "spec placeholders (SURVEY.md 8(d))"}
+
+
+def gram_sym_saving(dims, rank):
+    """sum_k s_k (s_k - 1) p_k: the FLOPs a symmetric Gram saves over the
+    reference's 2 s^2 p count (F_sym = F_ref - this)."""
+    n = len(dims)
+    T = math.prod(dims)
+    s = rank ** (n - 1)
+    return sum(s * (s - 1) * (T // d) for d in dims)
+
+
 def dist_env():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -353,6 +374,29 @@ def run_ours(args, wl, name):
                   "achieved_GBs": round(bst / (ms_step / 1e3) / 1e9, 1),
                   "frac": round(bst / (ms_step / 1e3) / 1e9 / pk["hbm_gbs"], 4),
                   "flops_ref_per_sweep": flops // args.steps}
+    # the compute half of the roofline: F_sym / (t P), P the
+    # measured FP64 peak (FP64 path) or TF32 tensor peak / 3 (3xTF32 products)
+    cp = compute_peaks()
+    f_sym = flops / args.steps - gram_sym_saving(wl.dims, wl.rank)
+    if b == 8:
+        p_tf, p_kind = cp["fp64_tflops"], "fp64 (DGEMM peak)"
+    else:
+        p_tf, p_kind = cp["tf32_tensor_tflops"] / 3.0, "tf32 tensor peak / 3 (3xTF32 products)"
+    c_tf = f_sym / (ms_step / 1e3) / 1e12
+    sweep_roof["F_sym_GFLOP"] = round(f_sym / 1e9, 3)
+    sweep_roof["compute_achieved_tflops"] = round(c_tf, 2)
+    sweep_roof["compute_peak_tflops"] = round(p_tf, 2)
+    sweep_roof["compute_peak_kind"] = p_kind
+    sweep_roof["compute_peak_source"] = cp["source"]
+    sweep_roof["compute_frac"] = round(c_tf / p_tf, 4)
+    sweep_roof["bound"] = "hbm" if sweep_roof["frac"] >= sweep_roof["compute_frac"] else p_kind.split()[0]
+    sweep_roof["achieved"] = max(sweep_roof["frac"], sweep_roof["compute_frac"])
+    # bytes the schedule as built moves (per-class algorithmic bytes of the
+    # profiled pass): the N = 3 Z route reads X twice, not N times, so this
+    # is below B_stream
+    sched = sum(v["bytes"] for v in prof.values()) / prof_steps
+    sweep_roof["schedule_GB"] = round(sched / 1e9, 4)
+    sweep_roof["schedule_frac"] = round(sched / (ms_step / 1e3) / 1e9 / pk["hbm_gbs"], 4)
     sweep_roof["host_wall_ms_per_step"] = round(host_ms / args.steps, 4)
     sweep_roof["sweep_event_ms_median"] = round(float(np.median(dev_ms)), 4)
     sweep_roof["profiled_pass_ms_per_step"] = round(prof_ms / prof_steps, 4)

@@ -1122,7 +1122,8 @@ class Ctx : public Executor {
     for (int j = 0; j < k; ++j) P *= sh.dims[j];
     int nb;
     int pm = pbegin(FCTN_K_COMPOSE);
-    if (dtype == FCTN_F32 && use_tc && tc_compose_supported(I, P, p, S)) {
+    const bool tc = dtype == FCTN_F32 && use_tc && tc_compose_supported(I, P, p, S);
+    if (tc) {
       // pre-split the small operands in HBM (A_(k) always; M_k when it is at
       // most a quarter of X) so the kernel converts only what streams
       ComposeOperands op;
@@ -1154,7 +1155,9 @@ class Ctx : public Executor {
     launch_reduce4(partials, nb, dstats + 3 * sh.n, st);
     allreduce_sum(dstats + 3 * sh.n, 4);  // the four sums over all slabs
     launches += 2;
-    pend(pm, objective_only ? (double)esize * (S * p + T) : (double)esize * (S * p + 2 * T) + (double)T, 2);
+    // mask: 1 bit per entry on the tensor-core path, 1 byte on the SIMT path
+    const double mask_bytes = objective_only ? 0.0 : (tc ? (double)T / 8.0 : (double)T);
+    pend(pm, objective_only ? (double)esize * (S * p + T) : (double)esize * (S * p + 2 * T) + mask_bytes, 2);
   }
 
   void fetch_stats() {
