@@ -14,7 +14,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libfctn_b200.so")
-SOURCES = ["kernels.cu", "stream.cu", "solve.cu", "eigh.cu", "compose.cu", "stream_tc.cu", "compose_tc.cu", "metrics.cu", "join.cu", "join_tc.cu", "fctn_ctx.cu", "plan.cpp"]
+SOURCES = ["kernels.cu", "stream.cu", "solve.cu", "eigh.cu", "tri.cu", "compose.cu", "stream_tc.cu", "compose_tc.cu", "metrics.cu", "join.cu", "join_tc.cu", "fctn_ctx.cu", "plan.cpp"]
 HEADERS = ["kernels.cuh", "tc_common.cuh", "plan.hpp", "executor.hpp", "../../include/fctn_b200.h"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

@@ -133,24 +133,39 @@ class Ctx : public Executor {
   double* dft_gscr = nullptr;  // column work arrays of long-mode DFTs (I > 4266)
   cudaStream_t st2 = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
-  int solve_pref = 0;  // FCTN_SOLVE: 0 auto, 1 = "chol", 2 = "eigh"
+  int solve_pref = 0;  // FCTN_SOLVE: 0 auto, 1 = "chol", 2 = "eigh", 3 = "tri"
+  double *tri_d = nullptr, *tri_e = nullptr;  // T of the tridiagonal form
+  enum { FORM_CHOL = 0, FORM_EIGH = 1, FORM_TRI = 2 };
   // Which form solves update k.  The eigenbasis form (eigh.cu, the
   // reference's own) runs on a side stream concurrently with the Y_k pass, so
   // it is off the critical path when its single-SM Jacobi is shorter than
   // that pass.  s > 160 has no Cholesky kernel: always eigh (from global
   // memory above s = 117).  The choice depends only on global shapes and the
   // visiting order, so every rank of a sharded run makes the same one.
-  bool eigh_for(int k, bool long_y) const {
-    const int64_t S = gsh.s_of(k);
-    if (S > 160) return true;
-    if (solve_pref == 1 || !eigh_fits_smem(S)) return false;
-    if (solve_pref == 2) return true;
-    // auto: measured on B200 the single-SM Jacobi (c4 s = 64: ~0.6 ms warm,
-    // c5 s = 81: ~1.2 ms) exceeds the Y_k passes it would hide under, while
-    // the all-SM Cholesky takes 0.08 ms; keep the Cholesky form
+  //
+  // Three exact forms:
+  //   chol (solve.cu) per-frequency Cholesky of G + mu_w I over all SMs --
+  //                   the default for s <= 160;
+  //   eigh (eigh.cu)  Jacobi eigendecomposition G = V diag(phi) V^T, the
+  //                   reference's literal form: s > 160 (from global memory)
+  //                   or FCTN_SOLVE=eigh;
+  //   tri  (tri.cu)   G = Q T Q^T, per-frequency tridiagonal solves
+  //                   (FCTN_SOLVE=tri).
+  // eigh and tri decompose G once per update on the side stream, off the
+  // critical path in principle, but their single-CTA FP64 kernels are
+  // latency bound on B200 (c4, s = 64: Jacobi ~0.6 ms warm, tridiagonal
+  // 0.28 ms) against 0.105 ms for all 1025 Cholesky systems, and the
+  // update's Y_k pass does not hide them; measured sweep c4: chol 1.48 ms,
+  // tri 1.86 ms, eigh 2.1 ms.
+  int form_for(int k, bool long_y) const {
     (void)long_y;
-    return false;
+    const int64_t S = gsh.s_of(k);
+    if (S > 160) return FORM_EIGH;
+    if (solve_pref == 2) return eigh_fits_smem(S) ? FORM_EIGH : FORM_CHOL;
+    if (solve_pref == 3) return tridiag_fits_smem(S) ? FORM_TRI : FORM_CHOL;
+    return FORM_CHOL;
   }
+  bool eigh_for(int k, bool long_y) const { return form_for(k, long_y) != FORM_CHOL; }
   double* dstats = nullptr;  // [n*3 factor stats][4 sums]
   int* dstatus = nullptr;
   double* hstats = nullptr;  // pinned mirror (+ status)
@@ -399,8 +414,8 @@ class Ctx : public Executor {
     E64.clear();
     for (auto* p : Vb) cudaFree(p);
     Vb.clear();
-    for (auto* p : {phi, Ytmp, ework, dft_gscr}) cudaFree(p);
-    phi = Ytmp = ework = dft_gscr = nullptr;
+    for (auto* p : {phi, Ytmp, ework, dft_gscr, tri_d, tri_e}) cudaFree(p);
+    phi = Ytmp = ework = dft_gscr = tri_d = tri_e = nullptr;
     Ascratch = nullptr;
     Mbuf = nullptr;
     Y = G = Fr = Fi = ypart = partials = epart = colstats = gnet[0] = gnet[1] = nullptr;
@@ -526,6 +541,8 @@ class Ctx : public Executor {
     CK(cudaMalloc(&Y, max_is * sizeof(double)));
     CK(cudaMalloc(&Ytmp, max_is * sizeof(double)));
     CK(cudaMalloc(&phi, max_s * sizeof(double)));
+    CK(cudaMalloc(&tri_d, max_s * sizeof(double)));
+    CK(cudaMalloc(&tri_e, max_s * sizeof(double)));
     Vb.assign(n, nullptr);
     for (int k = 0; k < n; ++k) {
       const int64_t S = gsh.s_of(k);
@@ -755,7 +772,7 @@ class Ctx : public Executor {
     {
       const char* sv = getenv("FCTN_SOLVE");
       const std::string v = sv ? sv : "";
-      solve_pref = v == "chol" ? 1 : v == "eigh" ? 2 : 0;
+      solve_pref = v == "chol" ? 1 : v == "eigh" ? 2 : v == "tri" ? 3 : 0;
     }
     {
       cudaMemPool_t pool;
@@ -984,10 +1001,10 @@ class Ctx : public Executor {
 
   void factor_update(int k, int zj, int extrap, double alpha, double beta) {
     const bool long_y = zj < 0 || zver[zj] != planner->versions[zj];
-    const bool eg = eigh_for(k, long_y);
-    if (eg) {
-      // G_k and its eigendecomposition need only the other factors' Grams:
-      // run them on the side stream while this stream forms Y_k
+    const int form = form_for(k, long_y);
+    if (form != FORM_CHOL) {
+      // G_k and its decomposition need only the other factors' Grams: run
+      // them on the side stream while this stream forms Y_k
       CK(cudaEventRecord(ev_fork, st));
       CK(cudaStreamWaitEvent(st2, ev_fork, 0));
       const int64_t S = gsh.s_of(k);
@@ -996,7 +1013,15 @@ class Ctx : public Executor {
       gram_network(k, st2);
       pend(pm, 8.0 * S * S, launches - l0);
       pm = pbegin(FCTN_K_EIGH, st2);
-      launch_eigh(G, S, Vb[k], phi, ework, floor_shift[k], dstatus, 40, st2);
+      if (form == FORM_EIGH) {
+        launch_eigh(G, S, Vb[k], phi, ework, floor_shift[k], dstatus, 40, st2);
+      } else {
+        launch_tridiag(G, S, Vb[k], tri_d, tri_e, st2);
+        if (std::isfinite(check_mu[k])) {  // T-floor test (sylvester.py:108-113): G + check_mu I must be PD
+          launch_chol_solve(G, S, 0, mu[k], Fr, Fi, check_mu[k], dstatus, st2);
+          ++launches;
+        }
+      }
       ++launches;
       pend(pm, 8.0 * 3 * S * S, 1);
       CK(cudaEventRecord(ev_join, st2));
@@ -1007,7 +1032,7 @@ class Ctx : public Executor {
     } else {
       y_stream(k);
     }
-    solve_factor(k, eg, extrap, alpha, beta);
+    solve_factor(k, form, extrap, alpha, beta);
   }
 
   void y_stream(int k) {
@@ -1056,7 +1081,7 @@ class Ctx : public Executor {
     if (sharded()) finish_y(k, k == 0);
   }
 
-  void solve_factor(int k, bool eg, int extrap, double alpha, double beta) {
+  void solve_factor(int k, int form, int extrap, double alpha, double beta) {
     const int64_t T = gsh.total();
     const int64_t I = gsh.dims[k], S = gsh.s_of(k), p = T / I;
     planner->meter.proj += 2 * I * p * S;   // sylvester.py:105
@@ -1064,15 +1089,20 @@ class Ctx : public Executor {
     const DftPlan& dp = dft[k];
     const double sgn = sign == FCTN_SIGN_PD ? -1.0 : 1.0;
     int pm;
-    if (eg) {
+    if (form != FORM_CHOL) {
       // the reference's closed form (sylvester.py:108-116) in the basis from
-      // the side stream: A = Re(F^H [(F (Y V)) / T]) V^T
+      // the side stream: A = Re(F^H [(F (Y V)) / T]) V^T (eigh: T diagonal;
+      // tri: V = Q, per-frequency tridiagonal solves instead of the divide)
       CK(cudaStreamWaitEvent(st, ev_join, 0));
       pm = pbegin(FCTN_K_DFT);
       launch_rotate<double>(Y, I, S, Vb[k], false, Ytmp, nullptr, 0, 0.0, 0.0, (double*)nullptr, st);
       launch_dft_fwd(Ytmp, dp, S, cosT[k], sinT[k], Fr, Fi, st, dft_gscr);
+      if (form == FORM_TRI) {
+        launch_thomas(tri_d, tri_e, S, dp.H1, mu[k], Fr, Fi, dstatus, st);
+        ++launches;
+      }
       launch_dft_inv<double>(Fr, Fi, dp, S, cosT[k], sinT[k], nullptr, Ytmp, (double*)nullptr, 0, 0.0, 0.0,
-                             delta[k], sgn, nullptr, st, mu[k], phi, dft_gscr);
+                             delta[k], sgn, nullptr, st, mu[k], form == FORM_EIGH ? phi : nullptr, dft_gscr);
       if (dtype == FCTN_F64)
         launch_rotate<double>(Ytmp, I, S, Vb[k], true, Ascratch, A64[k], extrap, alpha, beta, (double*)nullptr, st);
       else
@@ -1184,7 +1214,7 @@ class Ctx : public Executor {
     const int n = sh.n;
     const std::vector<int> route = plan_routes(order);
     bool side = false;
-    for (int k = 0; k < n; ++k) side |= eigh_for(k, true);
+    for (int k = 0; k < n; ++k) side |= form_for(k, true) != FORM_CHOL;
     tc_reserve_sms(side ? 1 : 0);  // one SM for the concurrent eigendecomposition
     for (size_t t = 0; t < order.size(); ++t) {
       const int k = order[t];

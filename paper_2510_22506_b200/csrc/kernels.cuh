@@ -145,6 +145,14 @@ template <typename T>
 void launch_rotate(const double* A, int64_t I, int64_t S, const double* V, bool trans, double* out,
                    const double* aold, int extrap, double alpha, double beta, T* acomp, cudaStream_t st);
 void launch_identity(double* V, int64_t S, cudaStream_t st);
+// tridiagonal form of the solve (tri.cu): G = Q T Q^T (d: diagonal, e:
+// sub-diagonal of T) in one CTA; per-frequency Thomas solves of
+// (T + mu_w I) x = F_w in place on (Fr, Fi) (status |= 2 on a non-positive pivot)
+size_t tridiag_smem_bytes(int64_t S);
+bool tridiag_fits_smem(int64_t S);
+void launch_tridiag(const double* G, int64_t S, double* Q, double* d, double* e, cudaStream_t st);
+void launch_thomas(const double* d, const double* e, int64_t S, int64_t H1, const double* mu, double* Fr, double* Fi,
+                   int* status, cudaStream_t st);
 // [||a - a_old||^2, ||a||^2, a.(L a)] per column
 void launch_colstats3(const double* A, const double* Aold, int64_t I, int64_t S, double delta, double sgn,
                       double* colstats, cudaStream_t st);

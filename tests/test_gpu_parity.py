@@ -199,13 +199,14 @@ def test_gpu_split_dft_fp64(dims, rank):
         assert a.step_sq == pytest.approx(b.step_sq, rel=1e-6, abs=1e-12)
 
 
-@pytest.mark.parametrize("solve", ["eigh", "chol"])
+@pytest.mark.parametrize("solve", ["eigh", "chol", "tri"])
 @pytest.mark.parametrize("name", ["n3_afctnlr", "n4_afctnlr_shuffle", "n5_budget_binds", "n3_extrapolation",
                                   "n4_nonuniform_rank", "c3_scaled"])
 def test_gpu_solve_forms_match_reference_golden(monkeypatch, name, solve):
-    """Both device forms of the factor subproblem against the reference:
-    the eigenbasis form (eigh.cu, the reference's own sylvester.py:51-61,
-    98-116) and the per-frequency Cholesky form, forced for every update."""
+    """Every device form of the factor subproblem against the reference,
+    forced for every update: the eigenbasis form (eigh.cu, the reference's
+    own sylvester.py:51-61, 98-116), the per-frequency Cholesky form and the
+    tridiagonal form (tri.cu)."""
     monkeypatch.setenv("FCTN_SOLVE", solve)
     case = load_run(name)
     res = P.run(P.Observation(case["values"], case["mask"]), _cfg(case["config"]))
