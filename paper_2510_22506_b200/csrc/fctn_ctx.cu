@@ -10,6 +10,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <map>
@@ -44,7 +45,9 @@ struct CudaError : std::runtime_error {
       throw ::fctn::CudaError(std::string(#call) + " failed: " + cudaGetErrorString(_e));            \
   } while (0)
 
-static const int64_t M_ID = 0;  // fixed executor id of the M_k buffer
+static const int64_t M_ID = 0;    // fixed executor id of the M_k buffer
+static const int64_t X_ID = -10;  // the current iterate X (labels 0 .. n-1, first fastest)
+static const int64_t Y_ID = -11;  // the fp64 Y_k buffer (labels [k, bonds to k])
 
 // Collectives of the mode-0 sharded sweep: NCCL on the
 // context stream (resolved at run time from the process's libnccl, so the
@@ -182,6 +185,11 @@ class Ctx : public Executor {
   int64_t ypart_cap = 0;        // doubles in ypart
   int mbuf_holds = -1;   // mode whose M_k currently sits in Mbuf (-1: none)
   bool zroute = true;    // FCTN_NO_ZROUTE=1 disables
+  // Y_k without M_k (alt_join): armed per update by sweep_device
+  bool alt_route = true;  // FCTN_NO_ALTJOIN=1 disables
+  bool alt_ok = false;
+  int alt_k = -1;
+  bool y_ready = false;
   // Three-mode sweeps have no data-dependent host decisions and no allocations,
   // so each (visiting order, X buffer parity, extrapolation) sweep is captured
   // once as a CUDA graph and replayed (FCTN_NO_GRAPH=1 disables).
@@ -275,6 +283,8 @@ class Ctx : public Executor {
   void* ptr_of(const LTensor& t) {
     if (t.factor >= 0) return const_cast<void*>(fac_ptr(t.factor));
     if (t.buf == M_ID) return Mbuf;
+    if (t.buf == X_ID) return X[cur];
+    if (t.buf == Y_ID) return Y;
     auto it = bufs.find(t.buf);
     if (it == bufs.end()) throw std::runtime_error("unknown buffer id");
     return it->second;
@@ -586,6 +596,7 @@ class Ctx : public Executor {
     std::vector<int64_t> versions = planner ? planner->versions : std::vector<int64_t>(n, 0);
     planner.reset(new Planner(gsh, budget));  // the reference's chain and budget are global
     planner->versions = versions;
+    planner->final_join_hook = [this](const LTensor& l, const LTensor& r) { return alt_join(l, r); };
   }
 
   // ------------------------------------------------------------ collectives
@@ -760,6 +771,8 @@ class Ctx : public Executor {
       use_graph = !(ng && ng[0] == '1');
       const char* zr = getenv("FCTN_NO_ZROUTE");
       zroute = !(zr && zr[0] == '1');
+      const char* aj = getenv("FCTN_NO_ALTJOIN");
+      alt_route = !(aj && aj[0] == '1');
       const char* t = getenv("FCTN_TF32");
       split3 = !(t && std::string(t) == "1x");
     }
@@ -999,6 +1012,115 @@ class Ctx : public Executor {
     mbuf_holds = k;
   }
 
+  // Y_k without M_k.  The reference forms M_k = left (*) right (the final
+  // join, network.py:493-497) and then Y_k = X_(k) M_k^T (sylvester.py:104).
+  // When M_k is far larger than X (c3's 3-extent colour mode: |M_2| = 158 M
+  // entries against T = 3.8 M) the same sums are cheaper in another
+  // association: W = X (*) F over F's physical modes (F the partial whose
+  // W is smaller), then Y_k = W (*) (the other partial) over the remaining
+  // physical modes and the bonds between the partials.  Nothing of size M_k
+  // is written (c3 mode 2: W has 9.5 M entries, 1.9 GFLOP instead of 8.9).
+  // Used when M_k is not needed afterwards (k is not the order's last mode:
+  // the compose reads M_last) on the FP64, unsharded path; the FLOP meter
+  // still records the reference's join (plan.cpp).
+  bool alt_join(const LTensor& left, const LTensor& right) {
+    if (!alt_ok || !alt_route) return false;
+    const int k = alt_k;
+    const int n = sh.n;
+    const int64_t T = sh.total(), I = sh.dims[k], S = sh.s_of(k);
+    const std::vector<int> kb = sh.bonds_of(k);
+    auto has = [](const std::vector<int>& v, int l) { return std::find(v.begin(), v.end(), l) != v.end(); };
+    std::vector<int> shared;
+    for (int l : left.labels)
+      if (!sh.is_phys(l) && has(right.labels, l)) shared.push_back(l);
+    int64_t rsz = 1;
+    for (int l : shared) rsz *= sh.extent(l);
+    auto side = [&](const LTensor& f, int64_t* psz, int64_t* ssz) {
+      *psz = 1;
+      *ssz = 1;
+      for (int l : f.labels) {
+        if (sh.is_phys(l)) *psz *= sh.extent(l);
+        else if (has(kb, l)) *ssz *= sh.extent(l);
+      }
+    };
+    int64_t pl, sl, pr, sr;
+    side(left, &pl, &sl);
+    side(right, &pr, &sr);
+    // cost model (FP64 SIMT contractions ~15 TFLOP/s, ~4 TB/s of traffic):
+    // current = join + stream with M_k written and read; alt-L / alt-R =
+    // X (*) left / right first
+    const double Fr_ = 15e12, Bw = 4e12;
+    const double ln = (double)left.numel(sh), rn = (double)right.numel(sh);
+    const double m_numel = (double)S * (double)(T / I);
+    const double cur = (2.0 * (double)(pl * sl) * (double)rsz * (double)(pr * sr) + 2.0 * (double)T * S) / Fr_ +
+                       8.0 * (ln + rn + 2.0 * m_numel + T) / Bw;
+    const double wl = (double)(T / pl) * sl * rsz, wr = (double)(T / pr) * sr * rsz;
+    const double alt_l = (2.0 * T * (double)(sl * rsz) + 2.0 * (double)(I * sl) * (double)(pr * rsz) * sr) / Fr_ +
+                         8.0 * (T + ln + 2.0 * wl + rn) / Bw;
+    const double alt_r = (2.0 * T * (double)(sr * rsz) + 2.0 * (double)(I * sr) * (double)(pl * rsz) * sl) / Fr_ +
+                         8.0 * (T + rn + 2.0 * wr + ln) / Bw;
+    const bool first_left = alt_l <= alt_r;
+    const double w_numel = first_left ? wl : wr;
+    if (std::min(alt_l, alt_r) > 0.5 * cur) return false;  // only when clearly cheaper
+    const LTensor& first = first_left ? left : right;
+    const LTensor& second = first_left ? right : left;
+    int pm = pbegin(FCTN_K_STREAM_Y);
+    // W = X (*) first
+    ContractOp op1;
+    op1.a.labels.resize(n);
+    for (int j = 0; j < n; ++j) op1.a.labels[j] = j;
+    op1.a.buf = X_ID;
+    op1.b = first;
+    for (int l : op1.a.labels)
+      if (!has(first.labels, l)) op1.out.labels.push_back(l);
+    for (int l : first.labels)
+      if (!has(op1.a.labels, l)) op1.out.labels.push_back(l);
+    std::sort(op1.out.labels.begin(), op1.out.labels.end());
+    ContractOp op2;
+    op2.a = op1.out;
+    op2.b = second;
+    op2.out.labels = sh.factor_labels(k);
+    op2.out.buf = Y_ID;
+    // both contractions must fit the generic kernel's split-K limits
+    // (kernels.cu launch_contract: K chunks <= 6144 from the scratch)
+    auto feasible = [&](const ContractOp& op) {
+      bool swp = false;
+      const ContractDesc dd = desc_for(op, &swp);
+      if (dd.K <= 6144) return true;
+      const int64_t tiles = ((dd.rows + 63) / 64) * ((dd.cols + 63) / 64);
+      const int64_t need = (dd.K + 6143) / 6144;
+      return tiles < n_sm && need * dd.rows * dd.cols <= cscratch_cap &&
+             need <= std::min<int64_t>(dd.K / 64, (2 * n_sm + tiles - 1) / tiles);
+    };
+    if (!feasible(op1) || !feasible(op2)) {
+      pend(pm, 0.0, 0);
+      return false;
+    }
+    op1.out.buf = alloc_labels(op1.out.labels);
+    op2.a.buf = op1.out.buf;
+    {
+      bool sw1 = false;
+      ContractDesc d1 = desc_for(op1, &sw1);
+      launch_contract<double>((const double*)ptr_of(sw1 ? op1.b : op1.a), (const double*)ptr_of(sw1 ? op1.a : op1.b),
+                              (double*)ptr_of(op1.out), d1, cscratch, cscratch_cap, n_sm, st);
+      ++launches;
+    }
+    // Y_k = W (*) second, [k, bonds to k] (split-K: the reduction runs over
+    // most of the tensor)
+    bool sw = false;
+    ContractDesc d = desc_for(op2, &sw);
+    const double* pa = (const double*)ptr_of(sw ? op2.b : op2.a);
+    const double* pb = (const double*)ptr_of(sw ? op2.a : op2.b);
+    launch_contract<double>(pa, pb, Y, d, cscratch, cscratch_cap, n_sm, st);
+    ++launches;
+    free(op1.out.buf);
+    launch_axpy(Y, A64[k], rho, I * S, st);  // + rho A_prev (sylvester.py:106)
+    ++launches;
+    pend(pm, 8.0 * (T + w_numel * 2 + ln + rn + 2.0 * I * S), 4);
+    y_ready = true;
+    return true;
+  }
+
   void factor_update(int k, int zj, int extrap, double alpha, double beta) {
     const bool long_y = zj < 0 || zver[zj] != planner->versions[zj];
     const int form = form_for(k, long_y);
@@ -1029,6 +1151,8 @@ class Ctx : public Executor {
     if (zj >= 0) {
       if (zver[zj] != planner->versions[zj]) compute_z(zj);
       y_from_z(zj, k);
+    } else if (y_ready) {
+      y_ready = false;  // formed by alt_join during the chain
     } else {
       y_stream(k);
     }
@@ -1219,12 +1343,16 @@ class Ctx : public Executor {
     for (size_t t = 0; t < order.size(); ++t) {
       const int k = order[t];
       const bool zr = route[t] >= 0;
+      y_ready = false;
+      alt_k = k;
+      alt_ok = dtype == FCTN_F64 && !sharded() && n >= 4 && k != order.back();
       if (alg == FCTN_ALG_ACCEL) {
         planner->partial_cached(k, order, zr ? nullptr : this, M_ID);  // dry replay when M_k is not needed
       } else {
         planner->partial_plain(k, zr ? nullptr : this, M_ID);
       }
-      mbuf_holds = zr ? -1 : k;
+      alt_ok = false;
+      mbuf_holds = (zr || y_ready) ? -1 : k;
       factor_update(k, route[t], extrap, alpha, beta);
     }
     int k_last = order.back();

@@ -8,6 +8,7 @@
 #pragma once
 
 #include <cstdint>
+#include <functional>
 #include <map>
 #include <string>
 #include <vector>
@@ -155,6 +156,11 @@ class Planner {
   ReuseCacheMirror& cache() { return cache_; }
   std::vector<int64_t> versions;  // per-factor version stamps
   Meter meter;
+  // Optional device-side replacement of the final join M_k = left (*) right
+  // (partial_cached): when it returns true it has consumed the two partials
+  // itself (e.g. formed Y_k without M_k); the planner still meters the
+  // reference's join FLOPs.
+  std::function<bool(const LTensor&, const LTensor&)> final_join_hook;
 
   // Build M_k in the M layout into executor buffer `m_buf` (accelerated
   // variant, given visiting order).  Returns number of contractions run.
