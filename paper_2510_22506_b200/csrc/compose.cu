@@ -12,6 +12,14 @@
 
 namespace fctn {
 
+// separately rounded multiply / add / divide (no FMA contraction)
+__device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double div_rn(double a, double b) { return __ddiv_rn(a, b); }
+__device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ float add_rn(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ float div_rn(float a, float b) { return __fdiv_rn(a, b); }
+
 static void check_launch(const char* what) {
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) throw std::runtime_error(std::string(what) + ": " + cudaGetErrorString(e));
@@ -86,10 +94,10 @@ __global__ void __launch_bounds__(256) k_compose(const T* __restrict__ A, const 
         if (mask[off]) {
           xn = x;  // observed entries restored bit for bit (solver.py:235-236)
         } else {
-          // (x*rho + c)/(1+rho) in the reference's operation order (solver.py:232-234)
-          T t = x * r;
-          t = t + c;
-          xn = t / onep;
+          // (x*rho + c)/(1+rho) in the reference's operation order and
+          // rounding (solver.py:232-234: multiply, add, divide, each rounded;
+          // the _rn intrinsics keep nvcc from contracting them into an FMA)
+          xn = div_rn(add_rn(mul_rn(x, r), c), onep);
         }
         Xn[off] = xn;
         const double dx = (double)xn - (double)x;

@@ -497,7 +497,7 @@ void launch_scatter_rows(const double* g, int nranks, int64_t slab_max, int64_t 
 
 __global__ void k_axpy(double* __restrict__ y, const double* __restrict__ x, double a, int64_t n) {
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)
-    y[e] += a * x[e];
+    y[e] = __dadd_rn(y[e], __dmul_rn(a, x[e]));  // y += a x rounded like numpy (sylvester.py:106), no FMA
 }
 
 void launch_axpy(double* y, const double* x, double a, int64_t n, cudaStream_t st) {
@@ -575,7 +575,7 @@ __global__ void __launch_bounds__(256, 2) k_yzl(const T* __restrict__ Z, const T
     double v = 0.0;
     for (int q = 0; q < 8; ++q) v += red[q][e];
     const int64_t yi = o + p.Io * (bz * p.yz + c * p.ya);
-    if (aprev) v += rho * aprev[yi];  // + rho A_prev (sylvester.py:106), unsplit case
+    if (aprev) v = __dadd_rn(v, __dmul_rn(rho, aprev[yi]));  // + rho A_prev (sylvester.py:106), unsplit; no FMA
     Y[yi] = v;
   }
 }

@@ -176,7 +176,7 @@ __global__ void __launch_bounds__(256) k_reduce_splits(const PT* __restrict__ pa
     double v = 0.0;
 #pragma unroll
     for (int q = 0; q < 8; ++q) v += red[q][lane];
-    if (aprev) v += rho * aprev[e];
+    if (aprev) v = __dadd_rn(v, __dmul_rn(rho, aprev[e]));  // y + rho a_prev rounded like numpy (no FMA)
     out[e] = v;
   }
 }

@@ -89,7 +89,19 @@ def ssim(x, ref, peak: float = 1.0, *, device: int = 0) -> float:
 
 
 def rel_err(x, ref, mask=None, *, device: int = 0) -> float:
-    """Relative Frobenius error, off the mask when given (metrics.py:69-92)."""
+    """Relative Frobenius error, off the mask when given (metrics.py:69-92).
+    Like the reference it takes tensors of any order: below two modes the
+    data is viewed as one (n, 1) slice (the error does not depend on slicing)."""
+    x, ref = np.asarray(x), np.asarray(ref)
+    if x.shape != ref.shape:
+        raise ValueError("tensors must have identical shapes")
+    if x.ndim < 2:
+        if mask is not None:
+            mask = np.asarray(mask, dtype=bool)
+            if mask.shape != x.shape:
+                raise ValueError("mask shape mismatch")
+            mask = mask.reshape((x.size, 1))
+        x, ref = x.reshape((x.size, 1)), ref.reshape((ref.size, 1))
     q = _sums(x, ref, mask, 1.0, device)
     if mask is None:
         return _rel(q[_native.Q_ERR_SQ], q[_native.Q_REF_SQ])

@@ -60,7 +60,7 @@ def sample_mask(dims, sample_rate: float, seed: int) -> np.ndarray:
         raise ValueError("sample_rate must lie in (0, 1]")
     count = int(round(sample_rate * total))
     if count < 1:
-        raise ValueError("sample rate keeps no entry")
+        raise ValueError(f"sample_rate {sample_rate} keeps no entry of {dims}")  # fileio.py:133
     pick = np.random.default_rng(seed).permutation(total)[:count]
     flat = np.zeros(total, dtype=bool)
     flat[pick] = True

@@ -122,3 +122,17 @@ def test_gpu_run_resident_quality_matches_downloaded(dtype):
     assert abs(last.psnr - ref.psnr) <= 1e-9 and abs(last.ssim - ref.ssim) <= 1e-10
     assert last.rel_err == pytest.approx(ref.rel_err, rel=1e-10)
     assert abs(last.psnr - O.psnr(res.x, truth)) <= 1e-9
+
+
+@pytest.mark.gpu
+def test_rel_err_any_order_like_reference():
+    """rel_err accepts 1-D and 0-D tensors like the reference (metrics.py:70-92)."""
+    from paper_2510_22506_b200 import metrics as M
+    rng = np.random.default_rng(5)
+    a, b = rng.standard_normal(100), rng.standard_normal(100)
+    want = float(np.linalg.norm(a - b) / np.linalg.norm(b))
+    assert M.rel_err(a, b) == pytest.approx(want, rel=1e-12)
+    m = rng.random(100) < 0.3
+    want_m = float(np.linalg.norm(a[~m] - b[~m]) / np.linalg.norm(b[~m]))
+    assert M.rel_err(a, b, m) == pytest.approx(want_m, rel=1e-12)
+    assert M.rel_err(np.float64(2.0), np.float64(1.0)) == pytest.approx(1.0)
