@@ -596,7 +596,10 @@ class Ctx : public Executor {
     std::vector<int64_t> versions = planner ? planner->versions : std::vector<int64_t>(n, 0);
     planner.reset(new Planner(gsh, budget));  // the reference's chain and budget are global
     planner->versions = versions;
-    planner->final_join_hook = [this](const LTensor& l, const LTensor& r) { return alt_join(l, r); };
+    planner->final_join_hook = [this](const LTensor& l, const LTensor& r, const std::vector<int>& ls,
+                                      const std::vector<int>& rs) {
+      return alt_join(l, r) || reassoc_join(l, r, ls, rs);
+    };
   }
 
   // ------------------------------------------------------------ collectives
@@ -1118,6 +1121,79 @@ class Ctx : public Executor {
     ++launches;
     pend(pm, 8.0 * (T + w_numel * 2 + ln + rn + 2.0 * I * S), 4);
     y_ready = true;
+    return true;
+  }
+
+  // M_k in another association.  The reference's final join contracts two
+  // partials over every bond between them (c5, middle of the order: 2 + 2
+  // factors, K = 3^4 = 81 shared bonds, 20736 x 81 x 20736).  Absorbing the
+  // smaller side's factors one at a time into the other partial gives the
+  // same M_k with a K = 27 last step and an 81 M-entry intermediate (c5:
+  // 70 -> 23 GFLOP in the 430 M-entry output step); chosen by a cost model
+  // (tensor-core FLOPs at the 3xTF32 rate, bytes at HBM rate).
+  bool reassoc_join(const LTensor& left, const LTensor& right, const std::vector<int>& lseq,
+                    const std::vector<int>& rseq) {
+    if (!alt_route || sharded()) return false;
+    const bool absorb_right = rseq.size() <= lseq.size();
+    const std::vector<int>& fs = absorb_right ? rseq : lseq;
+    if (fs.size() != 2) return false;
+    const LTensor& base = absorb_right ? left : right;
+    const int k = alt_k;
+    auto has = [](const std::vector<int>& v, int l) { return std::find(v.begin(), v.end(), l) != v.end(); };
+    auto numel = [&](const std::vector<int>& ls) {
+      double e = 1;
+      for (int l : ls) e *= (double)sh.extent(l);
+      return e;
+    };
+    auto contracted = [&](const std::vector<int>& a, const std::vector<int>& b, double* kk) {
+      std::vector<int> out;
+      *kk = 1;
+      for (int l : a)
+        if (has(b, l)) *kk *= (double)sh.extent(l);
+        else out.push_back(l);
+      for (int l : b)
+        if (!has(a, l)) out.push_back(l);
+      std::sort(out.begin(), out.end());
+      return out;
+    };
+    const std::vector<int> mlab = sh.m_labels(k);
+    const double mn = numel(mlab);
+    double kjoin = 1;
+    contracted(left.labels, right.labels, &kjoin);
+    // pick the absorption order with the smaller intermediate
+    int first = fs[0], second = fs[1];
+    double k1 = 1, k1b = 1;
+    std::vector<int> t1 = contracted(base.labels, sh.factor_labels(first), &k1);
+    std::vector<int> t1b = contracted(base.labels, sh.factor_labels(second), &k1b);
+    if (numel(t1b) < numel(t1)) {
+      std::swap(first, second);
+      t1 = t1b;
+      k1 = k1b;
+    }
+    double k2 = 1;
+    contracted(t1, sh.factor_labels(second), &k2);
+    // join rates measured on B200 (c5 K = 27 / 81 joins: 0.48 / 1.1 ms for
+    // 430 M outputs): ~75 TFLOP/s effective for the 3xTF32 join, ~10 for the
+    // FP64 SIMT join; output stores at ~5 TB/s
+    const double b = (double)esize, F = dtype == FCTN_F32 ? 75e12 : 10e12, B = 5e12;
+    const double cur = 2.0 * mn * kjoin / F + b * mn / B;
+    const double alt = (2.0 * numel(t1) * k1 + 2.0 * mn * k2) / F + b * (2.0 * numel(t1) + mn) / B;
+    if (alt > 0.8 * cur || numel(t1) > 0.5 * mn) return false;
+    ContractOp op1;
+    op1.a = base;
+    op1.b.labels = sh.factor_labels(first);
+    op1.b.factor = first;
+    op1.out.labels = t1;
+    op1.out.buf = alloc_labels(t1);
+    contract(op1);
+    ContractOp op2;
+    op2.a = op1.out;
+    op2.b.labels = sh.factor_labels(second);
+    op2.b.factor = second;
+    op2.out.labels = mlab;
+    op2.out.buf = M_ID;
+    contract(op2);
+    free(op1.out.buf);
     return true;
   }
 

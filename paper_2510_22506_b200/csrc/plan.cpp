@@ -217,7 +217,7 @@ void Planner::partial_cached(int k, const std::vector<int>& order, Executor* exe
     return;
   }
   std::vector<int> mlab = sh_.m_labels(k);
-  if (exec && final_join_hook && final_join_hook(left, right))
+  if (exec && final_join_hook && final_join_hook(left, right, lseq, rseq))
     contract(left, right, nullptr, &mlab, m_buf, false);  // meter only (network.py:493-497)
   else
     contract(left, right, exec, &mlab, m_buf, false);  // network.py:493-497

@@ -157,10 +157,11 @@ class Planner {
   std::vector<int64_t> versions;  // per-factor version stamps
   Meter meter;
   // Optional device-side replacement of the final join M_k = left (*) right
-  // (partial_cached): when it returns true it has consumed the two partials
-  // itself (e.g. formed Y_k without M_k); the planner still meters the
-  // reference's join FLOPs.
-  std::function<bool(const LTensor&, const LTensor&)> final_join_hook;
+  // (partial_cached; lseq / rseq: the factors each side contracts): when it
+  // returns true it has done the work itself (formed Y_k without M_k, or M_k
+  // in another association); the planner still meters the reference's join.
+  std::function<bool(const LTensor&, const LTensor&, const std::vector<int>&, const std::vector<int>&)>
+      final_join_hook;
 
   // Build M_k in the M layout into executor buffer `m_buf` (accelerated
   // variant, given visiting order).  Returns number of contractions run.
