@@ -59,7 +59,9 @@ struct ComposeArgs {
   int nkb;                    // K blocks per tile (s padded to 32)
   int stages;
   int rows_are_p;
-  int prefetch;               // rows of a tile are contiguous in X: bulk-prefetch them to L2
+  int prefetch;               // L2 bulk prefetch of each tile's X_old: 1 rows contiguous per column,
+                              // 2 the tile's X block contiguous (rows = p, P == 1), 3 rows = p in
+                              // runs of P (P % 128 != 0)
   int a_pre, b_pre;           // operand arrives pre-split (hi and lo tensors) from HBM
   float rho, onep, inv_onep;
   int objective_only;
@@ -151,7 +153,35 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
       }
       __syncwarp();
-      if (args.prefetch) {
+      if (args.prefetch == 2) {
+        // rows = p with P == 1: the tile's X_old is one contiguous block of
+        // nrow * I entries (and nrow * I bits of mask)
+        const long long nrow = args.rows - r0 < 128 ? args.rows - r0 : 128;
+        const long long base = (long long)r0 * args.I, cnt = nrow * args.I;
+        const long long b0 = (base * 4) & ~15LL, b1 = ((base + cnt) * 4 + 15) & ~15LL;
+        for (long long o = b0 + (long long)lane * 1024; o < b1; o += 32 * 1024)
+          prefetch_l2(reinterpret_cast<const char*>(args.Xo) + o, (uint32_t)(b1 - o < 1024 ? b1 - o : 1024));
+        if (!args.objective_only && lane == 0) {
+          const long long w0 = (base >> 5) & ~3LL, w1 = ((base + cnt + 31) >> 5) + 4;
+          prefetch_l2(args.maskbits + w0, (uint32_t)(((w1 - w0) * 4 + 15) & ~15LL));
+        }
+      } else if (args.prefetch == 3) {
+        // rows = p in runs of P (not 128-aligned): prefetch run segment by segment
+        const long long nrow = args.rows - r0 < 128 ? args.rows - r0 : 128;
+        for (long long r = r0; r < r0 + nrow;) {
+          const long long in = r % args.P;
+          const long long seg = (args.P - in) < (r0 + nrow - r) ? (args.P - in) : (r0 + nrow - r);
+          const long long rb = in + args.PI * (r / args.P);
+          for (int c = lane; c < N; c += 32) {
+            const long long gc = c0 + c;
+            if (gc >= args.cols) break;
+            const long long off = rb + args.P * gc;
+            const long long b0 = (off * 4) & ~15LL, b1 = ((off + seg) * 4 + 15) & ~15LL;
+            prefetch_l2(reinterpret_cast<const char*>(args.Xo) + b0, (uint32_t)(b1 - b0));
+          }
+          r += seg;
+        }
+      } else if (args.prefetch) {
         const long long rbase = args.rows_are_p ? (r0 % args.P) + args.PI * (r0 / args.P) : r0;
         const long long cstride = args.rows_are_p ? args.P : args.I;
         const long long nrow = args.rows - r0 < 128 ? args.rows - r0 : 128;
@@ -244,14 +274,34 @@ __global__ void __launch_bounds__(THREADS, 1)
         const long long off0 = rowbase + colstride * (cb + c0);
         const long long rem = args.cols - (cb + c0);
         const int nc = rem < 16 ? (int)rem : 16;
+        // a row's 16 columns contiguous and 16-B aligned (rows = p with P == 1,
+        // c5's k = 0): four 16-B loads instead of sixteen 4-B ones
+        const bool vec = colstride == 1 && nc == 16 && (off0 & 3) == 0;
+        if (vec && row_ok) {
+          const float4* src = reinterpret_cast<const float4*>(args.Xo + off0);
 #pragma unroll
-        for (int q = 0; q < 16; ++q) {  // all loads in flight before the TMEM wait
-          const long long off = off0 + colstride * q;
-          x[q] = (row_ok && q < nc) ? __ldcs(args.Xo + off) : 0.0f;
-          mw[q] = (row_ok && q < nc && !args.objective_only) ? __ldg(args.maskbits + (off >> 5)) : 0u;
+          for (int v = 0; v < 4; ++v) {
+            const float4 t = __ldcs(src + v);
+            x[4 * v] = t.x;
+            x[4 * v + 1] = t.y;
+            x[4 * v + 2] = t.z;
+            x[4 * v + 3] = t.w;
+          }
+          const uint32_t w0 = args.objective_only ? 0u : __ldg(args.maskbits + (off0 >> 5));
+          const uint32_t w1 = args.objective_only ? 0u : __ldg(args.maskbits + ((off0 + 15) >> 5));
+#pragma unroll
+          for (int q = 0; q < 16; ++q) mw[q] = ((off0 + q) >> 5) == (off0 >> 5) ? w0 : w1;
+        } else {
+#pragma unroll
+          for (int q = 0; q < 16; ++q) {  // all loads in flight before the TMEM wait
+            const long long off = off0 + colstride * q;
+            x[q] = (row_ok && q < nc) ? __ldcs(args.Xo + off) : 0.0f;
+            mw[q] = (row_ok && q < nc && !args.objective_only) ? __ldg(args.maskbits + (off >> 5)) : 0u;
+          }
         }
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
         if (!row_ok) continue;
+        float xo[16];
 #pragma unroll
         for (int q = 0; q < 16; ++q) {
           if (q >= nc) break;
@@ -269,13 +319,19 @@ __global__ void __launch_bounds__(THREADS, 1)
               // multiplies by the rounded reciprocal (<= 1 ulp)
               xn = fmaf(x[q], args.rho, c) * args.inv_onep;
             }
-            __stcs(args.Xn + off, xn);
+            if (vec) xo[q] = xn;
+            else __stcs(args.Xn + off, xn);
             const float dx = xn - x[q], dc = xn - c;
             f_d += dx * dx;
             f_b += x[q] * x[q];
             f_c += dc * dc;
             f_n += xn * xn;
           }
+        }
+        if (vec && !args.objective_only) {
+          float4* dst = reinterpret_cast<float4*>(args.Xn + off0);
+#pragma unroll
+          for (int v = 0; v < 4; ++v) __stcs(dst + v, make_float4(xo[4 * v], xo[4 * v + 1], xo[4 * v + 2], xo[4 * v + 3]));
         }
       }
       s_d += (double)f_d;
@@ -720,7 +776,12 @@ int launch_compose_tc(const ComposeOperands& op, const float* Xo, const uint32_t
   a.PI = P * I;
   a.I = I;
   a.nkb = (int)((S + KB - 1) / KB);
-  a.rows_are_p = P > 1;
+  // accumulator rows = the contiguous axis of X_(k) when it spans a 128-row
+  // tile (i for k = 0, p for k > 0); a short mode 0 (I < 128, c5: 48) takes
+  // rows = p instead, so the MMA's 128 rows are all live (with rows = i only
+  // I of 128 were)
+  static const bool rows_i = getenv("FCTN_COMPOSE_ROWS_I") != nullptr;  // A/B: the former rows = i for k = 0
+  a.rows_are_p = P > 1 || (I < 128 && !rows_i);
   a.rho = (float)rho;
   a.onep = (float)(1.0 + rho);
   a.inv_onep = (float)(1.0 / (1.0 + rho));
@@ -735,7 +796,7 @@ int launch_compose_tc(const ComposeOperands& op, const float* Xo, const uint32_t
   a.n_rb = (a.rows + 127) / 128;
   // a tile's 128 rows are one contiguous run of X when rows = i, or rows = p
   // within one run of the fastest modes (P a multiple of 128)
-  a.prefetch = (!a.rows_are_p || P % 128 == 0) ? 1 : 0;
+  a.prefetch = (!a.rows_are_p || P % 128 == 0) ? 1 : (P == 1 ? 2 : 3);
   const long long n_cb = (a.cols + N - 1) / N;
   a.n_tiles = a.n_rb * n_cb;
   int grid = (int)std::min<long long>(a.n_tiles, n_sm);
