@@ -125,12 +125,33 @@ __global__ void __launch_bounds__(256) k_contract(const T* __restrict__ A, const
   }
 }
 
+// Split-K reduction: a CTA owns 32 consecutive outputs; its 8 warps take the
+// splits round-robin with two independent accumulators each (many splits over
+// a small output, e.g. 296 x 375 for c3's Y_2 = W (*) L, would otherwise be one
+// dependent chain of loads per thread), combined in warp order: a fixed
+// summation tree.
 template <typename T>
-__global__ void k_contract_reduce(const T* __restrict__ part, int nsplit, const ContractDesc d, T* __restrict__ C) {
+__global__ void __launch_bounds__(256) k_contract_reduce(const T* __restrict__ part, int nsplit, const ContractDesc d,
+                                                         T* __restrict__ C) {
+  __shared__ T red[8][33];
   const int64_t n = d.rows * d.cols;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t e = blockIdx.x * 32LL + lane;
+  T a0 = T(0), a1 = T(0);
+  if (e < n) {
+    int sp = w;
+    for (; sp + 8 < nsplit; sp += 16) {
+      a0 += part[(int64_t)sp * n + e];
+      a1 += part[(int64_t)(sp + 8) * n + e];
+    }
+    if (sp < nsplit) a0 += part[(int64_t)sp * n + e];
+  }
+  red[w][lane] = a0 + a1;
+  __syncthreads();
+  if (w == 0 && e < n) {
     T v = T(0);
-    for (int s = 0; s < nsplit; ++s) v += part[s * n + e];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) v += red[q][lane];
     int64_t x, rc, cc;
     md_offsets(e % d.rows, d.nr, d.r_ext, d.r_sa, d.r_sc, x, rc);
     md_offsets(e / d.rows, d.nc, d.c_ext, d.c_sb, d.c_sc, x, cc);
@@ -414,8 +435,7 @@ void launch_contract(const T* A, const T* B, T* C, const ContractDesc& d, T* scr
   check_launch("contract");
   if (ns > 1) {
     const int64_t n = d.rows * d.cols;
-    int64_t blocks = std::min<int64_t>((n + 255) / 256, 4 * n_sm);
-    k_contract_reduce<T><<<(unsigned)blocks, 256, 0, st>>>(scratch, (int)ns, d, C);
+    k_contract_reduce<T><<<(unsigned)((n + 31) / 32), 256, 0, st>>>(scratch, (int)ns, d, C);
     check_launch("contract_reduce");
   }
 }
