@@ -10,12 +10,21 @@
 // fp64 workhorse and the fallback for shapes TMA cannot describe.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+#include <cstdlib>
 #include <stdexcept>
+#include <type_traits>
 #include <string>
 
 #include "kernels.cuh"
 
 namespace fctn {
+
+#define CK_STREAM(x)                                                                          \
+  do {                                                                                        \
+    cudaError_t e_ = (x);                                                                     \
+    if (e_ != cudaSuccess) throw std::runtime_error(std::string(#x) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
 
 static void check_launch(const char* what) {
   cudaError_t e = cudaGetLastError();
@@ -135,9 +144,124 @@ static void stream_ri(const T* X, const T* M, double* part, int64_t I, int64_t P
     stream_go<T, TS, 4>(X, M, part, I, P, S, p, sp, st);
 }
 
+// FP64 on the tensor cores (DMMA: mma.sync.aligned.m8n8k4 f64, exact IEEE
+// double FMAs): the same split-K product for the FP64 path.  CTA = 64 rows
+// (mode k) x 64 bond columns x one p-chunk, 8 warps of 32 x 16; K stages of
+// 32 p staged in shared memory (padded leading dimensions: the fragment
+// reads are conflict-free at the 64-bit two-wavefront minimum).  Register
+// reuse: 4 A + 2 B fragments feed 8 DMMAs per K = 4 step, against one shared
+// load per 2 FMAs in the SIMT tile above (shared-memory bound at ~25 % of
+// the FP64 peak on c3).
+__device__ __forceinline__ void dmma_8x8x4(double (&d)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(d[0]), "+d"(d[1])
+               : "d"(a), "d"(b));
+}
+
+template <bool XFAST>
+__global__ void __launch_bounds__(256) k_stream_dmma(const double* __restrict__ X, const double* __restrict__ M,
+                                                     double* __restrict__ part, int64_t I, int64_t P, int64_t S,
+                                                     int64_t p, int64_t chunk) {
+  constexpr int BI = 64, BS = 64, KC = 32;
+  __shared__ double Xs[BI][KC + 4];  // [i][p]
+  __shared__ double Ms[KC][BS + 8];  // [p][s]
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int wi = w >> 2, ws = w & 3;  // warp tile: rows 32 wi .. +32, cols 16 ws .. +16
+  const int64_t i0 = (int64_t)blockIdx.x * BI, s0 = (int64_t)blockIdx.z * BS;
+  const int64_t split = blockIdx.y;
+  const int64_t pb = split * chunk;
+  int64_t pe = pb + chunk;
+  if (pe > p) pe = p;
+  const int64_t PI = P * I;
+  double acc[4][2][2];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 2; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+  for (int64_t p0 = pb; p0 < pe; p0 += KC) {
+#pragma unroll
+    for (int j = 0; j < (BI * KC) / 256; ++j) {
+      const int e = tid + 256 * j;
+      int il, pl;
+      if (XFAST) {
+        il = e % BI;
+        pl = e / BI;
+      } else {
+        pl = e % KC;
+        il = e / KC;
+      }
+      const int64_t gp = p0 + pl, gi = i0 + il;
+      double v = 0.0;
+      if (gp < pe && gi < I) v = X[XFAST ? gi + I * gp : (gp % P) + P * gi + PI * (gp / P)];
+      Xs[il][pl] = v;
+    }
+#pragma unroll
+    for (int j = 0; j < (KC * BS) / 256; ++j) {
+      const int e = tid + 256 * j;
+      const int pl = e % KC, sl = e / KC;
+      const int64_t gp = p0 + pl, gs = s0 + sl;
+      Ms[pl][sl] = (gp < pe && gs < S) ? M[gp + p * gs] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < KC; kk += 4) {
+      double av[4], bv[2];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) av[a] = Xs[32 * wi + 8 * a + (lane >> 2)][kk + (lane & 3)];
+#pragma unroll
+      for (int b = 0; b < 2; ++b) bv[b] = Ms[kk + (lane & 3)][16 * ws + 8 * b + (lane >> 2)];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 2; ++b) dmma_8x8x4(acc[a][b], av[a], bv[b]);
+    }
+    __syncthreads();
+  }
+  double* out = part + split * I * S;
+#pragma unroll
+  for (int a = 0; a < 4; ++a) {
+    const int64_t gi = i0 + 32 * wi + 8 * a + (lane >> 2);
+    if (gi >= I) continue;
+#pragma unroll
+    for (int b = 0; b < 2; ++b)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int64_t gs = s0 + 16 * ws + 8 * b + 2 * (lane & 3) + h;
+        if (gs < S) out[gi + I * gs] = acc[a][b][h];
+      }
+  }
+}
+
+// the DMMA form for the FP64 path when the tile is not mostly padding; it
+// uses at most the split count the SIMT plan reserved partials for
+static bool dmma_ok(int64_t I, int64_t S) {
+  static const bool off = getenv("FCTN_NO_DMMA") != nullptr;
+  return !off && I >= 16 && S >= 16;
+}
+
 template <typename T>
 void launch_stream(const T* X, const T* M, double* part, int64_t I, int64_t P, int64_t S, int64_t p,
                    const StreamPlan& sp, cudaStream_t st) {
+  if constexpr (std::is_same<T, double>::value) {
+    if (dmma_ok(I, S)) {
+      const int64_t ti = (I + 63) / 64, ts = (S + 63) / 64;
+      int64_t want = std::max<int64_t>(1, (2 * 148 + ti * ts - 1) / (ti * ts));
+      want = std::min<int64_t>(want, std::max<int64_t>(1, (p + 255) / 256));
+      want = std::min<int64_t>(want, sp.nsplit);  // the partial buffer is sized for sp.nsplit
+      int64_t chunk = (p + want - 1) / want;
+      chunk = (chunk + 31) / 32 * 32;
+      const int64_t ns = (p + chunk - 1) / chunk;
+      // k_reduce_splits reads sp.nsplit partials: zero the ones this grid leaves empty
+      if (ns < sp.nsplit) CK_STREAM(cudaMemsetAsync(part + ns * I * S, 0, (sp.nsplit - ns) * I * S * sizeof(double), st));
+      dim3 grid((unsigned)ti, (unsigned)ns, (unsigned)ts);
+      if (P == 1)
+        k_stream_dmma<true><<<grid, 256, 0, st>>>(X, M, part, I, P, S, p, chunk);
+      else
+        k_stream_dmma<false><<<grid, 256, 0, st>>>(X, M, part, I, P, S, p, chunk);
+      check_launch("stream_dmma");
+      return;
+    }
+  }
   switch (sp.ts) {
     case 16: stream_ri<T, 16>(X, M, part, I, P, S, p, sp, st); break;
     case 32: stream_ri<T, 32>(X, M, part, I, P, S, p, sp, st); break;

@@ -33,7 +33,10 @@ def test_stream_fp32_matches_numpy(dims, k, S, use_tc):
     assert err <= 1e-5, err
 
 
-@pytest.mark.parametrize("dims,k,S", [((30, 20, 10), 0, 16), ((30, 20, 10), 1, 36), ((7, 9, 5, 6), 2, 125)])
+@pytest.mark.parametrize("dims,k,S", [((30, 20, 10), 0, 16), ((30, 20, 10), 1, 36), ((7, 9, 5, 6), 2, 125),
+                                     # DMMA form (I, S >= 16): P == 1, P > 1, ragged tiles, several splits
+                                     ((144, 40, 6), 0, 125), ((36, 176, 5), 1, 125), ((9, 8, 50, 3), 2, 25),
+                                     ((64, 2048, 3), 1, 64)])
 def test_stream_fp64_matches_numpy(dims, k, S):
     rng = np.random.default_rng(4)
     x = np.asfortranarray(rng.standard_normal(dims))
