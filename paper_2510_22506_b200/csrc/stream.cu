@@ -179,6 +179,9 @@ __global__ void __launch_bounds__(256) k_stream_dmma(const double* __restrict__ 
 #pragma unroll
     for (int b = 0; b < 2; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
   for (int64_t p0 = pb; p0 < pe; p0 += KC) {
+    // p = (r, q) with r = p % P: one 64-bit division per stage, then at most
+    // one wrap inside the 32-wide stage when P >= 32
+    const int64_t q0 = XFAST ? 0 : p0 / P, r0 = XFAST ? 0 : p0 - q0 * P;
 #pragma unroll
     for (int j = 0; j < (BI * KC) / 256; ++j) {
       const int e = tid + 256 * j;
@@ -192,7 +195,23 @@ __global__ void __launch_bounds__(256) k_stream_dmma(const double* __restrict__ 
       }
       const int64_t gp = p0 + pl, gi = i0 + il;
       double v = 0.0;
-      if (gp < pe && gi < I) v = X[XFAST ? gi + I * gp : (gp % P) + P * gi + PI * (gp / P)];
+      if (gp < pe && gi < I) {
+        if (XFAST) {
+          v = X[gi + I * gp];
+        } else {
+          int64_t rr = r0 + pl, qq = q0;
+          if (P >= KC) {
+            if (rr >= P) {
+              rr -= P;
+              ++qq;
+            }
+          } else {
+            qq += rr / P;
+            rr %= P;
+          }
+          v = X[rr + P * gi + PI * qq];
+        }
+      }
       Xs[il][pl] = v;
     }
 #pragma unroll
