@@ -125,6 +125,104 @@ __global__ void __launch_bounds__(256) k_contract(const T* __restrict__ A, const
   }
 }
 
+// FP64 contraction on the tensor cores (DMMA, mma.sync m8n8k4 f64): the same
+// descriptor-driven tile (64 x 64 output, offset tables in shared memory) as
+// k_contract, with 8 warps of 32 x 16 and 4 A + 2 B fragments feeding 8
+// DMMAs per K = 4 step (the SIMT tile is shared-memory bound at ~2 TFLOP/s on
+// c3's joins).  Padded K-major stages keep fragment reads at the 64-bit
+// two-wavefront minimum.
+__device__ __forceinline__ void dmma_884(double (&d)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(d[0]), "+d"(d[1])
+               : "d"(a), "d"(b));
+}
+
+__global__ void __launch_bounds__(256) k_contract_dmma(const double* __restrict__ A, const double* __restrict__ B,
+                                                       double* __restrict__ C, double* __restrict__ part,
+                                                       const ContractDesc d, int64_t tiles_r, int64_t kchunk) {
+  constexpr int BR = 64, BC = 64, KC = 16, LD = 72;
+  __shared__ double As[KC][LD];
+  __shared__ double Bs[KC][LD];
+  __shared__ int64_t sRA[BR], sRC[BR], sCB[BC], sCC[BC];
+  extern __shared__ int64_t sK[];  // [kA | kB] for this CTA's K range
+  const int64_t tile = blockIdx.x;
+  const int64_t r0 = (tile % tiles_r) * BR;
+  const int64_t c0 = (tile / tiles_r) * BC;
+  const int64_t kb = blockIdx.y * kchunk;
+  int64_t ke = kb + kchunk;
+  if (ke > d.K) ke = d.K;
+  const int64_t nk = ke - kb;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int wr = w >> 2, wc = w & 3;  // warp tile: rows 32 wr .. +32, cols 16 wc .. +16
+  if (tid < BR) {
+    const int64_t r = r0 + tid;
+    int64_t oa = -1, oc = 0;
+    if (r < d.rows) md_offsets(r, d.nr, d.r_ext, d.r_sa, d.r_sc, oa, oc);
+    sRA[tid] = oa;
+    sRC[tid] = oc;
+  } else if (tid < BR + BC) {
+    const int c = tid - BR;
+    int64_t ob = -1, oc = 0;
+    if (c0 + c < d.cols) md_offsets(c0 + c, d.nc, d.c_ext, d.c_sb, d.c_sc, ob, oc);
+    sCB[c] = ob;
+    sCC[c] = oc;
+  }
+  for (int64_t k = tid; k < nk; k += 256) {
+    int64_t oa, ob;
+    md_offsets(kb + k, d.nk, d.k_ext, d.k_sa, d.k_sb, oa, ob);
+    sK[k] = oa;
+    sK[nk + k] = ob;
+  }
+  __syncthreads();
+  double acc[4][2][2];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 2; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+  for (int64_t k0 = 0; k0 < nk; k0 += KC) {
+    for (int e = tid; e < KC * BR; e += 256) {
+      const int kk = e / BR, r = e % BR;
+      const int64_t ra = sRA[r];
+      As[kk][r] = (ra >= 0 && k0 + kk < nk) ? A[ra + sK[k0 + kk]] : 0.0;
+    }
+    for (int e = tid; e < KC * BC; e += 256) {
+      const int kk = e / BC, c = e % BC;
+      const int64_t cb = sCB[c];
+      Bs[kk][c] = (cb >= 0 && k0 + kk < nk) ? B[cb + sK[nk + k0 + kk]] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < KC; kk += 4) {
+      double av[4], bv[2];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) av[a] = As[kk + (lane & 3)][32 * wr + 8 * a + (lane >> 2)];
+#pragma unroll
+      for (int b = 0; b < 2; ++b) bv[b] = Bs[kk + (lane & 3)][16 * wc + 8 * b + (lane >> 2)];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 2; ++b) dmma_884(acc[a][b], av[a], bv[b]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int a = 0; a < 4; ++a) {
+    const int rl = 32 * wr + 8 * a + (lane >> 2);
+    if (r0 + rl >= d.rows) continue;
+#pragma unroll
+    for (int b = 0; b < 2; ++b)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int cl = 16 * wc + 8 * b + 2 * (lane & 3) + h;
+        if (c0 + cl >= d.cols) continue;
+        if (part)
+          part[blockIdx.y * d.rows * d.cols + (r0 + rl) + d.rows * (c0 + cl)] = acc[a][b][h];
+        else
+          C[sRC[rl] + sCC[cl]] = acc[a][b][h];
+      }
+  }
+}
+
 // Split-K reduction: a CTA owns 32 consecutive outputs; its 8 warps take the
 // splits round-robin with two independent accumulators each (many splits over
 // a small output, e.g. 296 x 375 for c3's Y_2 = W (*) L, would otherwise be one
@@ -416,6 +514,10 @@ void launch_contract(const T* A, const T* B, T* C, const ContractDesc& d, T* scr
     return;
   }
   if (contract_resident<T>(A, B, C, d, n_sm, st)) return;
+  // what the specialised forms above do not take: FP64 on the tensor cores
+  // (measured faster than the SIMT tile, slower than k_join on the joins)
+  static const bool no_dmma = getenv("FCTN_NO_DMMA") != nullptr;
+  const bool dmma = std::is_same<T, double>::value && !no_dmma && d.rows >= 16 && d.cols >= 16 && d.K >= 4;
   int64_t ns = 1;
   if (scratch && tiles < n_sm && d.K >= 256) {
     ns = std::min<int64_t>(d.K / 64, (2 * n_sm + tiles - 1) / tiles);
@@ -431,8 +533,21 @@ void launch_contract(const T* A, const T* B, T* C, const ContractDesc& d, T* scr
     if (e != cudaSuccess) throw std::runtime_error(std::string("contract smem: ") + cudaGetErrorString(e));
   }
   dim3 grid((unsigned)tiles, (unsigned)ns);
-  k_contract<T><<<grid, 256, smem, st>>>(A, B, C, ns > 1 ? scratch : nullptr, d, tr, kchunk);
-  check_launch("contract");
+  if constexpr (std::is_same<T, double>::value) {
+    if (dmma) {
+      if (smem > 24 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(k_contract_dmma, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem + 1024);
+        if (e != cudaSuccess) throw std::runtime_error(std::string("contract_dmma smem: ") + cudaGetErrorString(e));
+      }
+      k_contract_dmma<<<grid, 256, smem, st>>>(A, B, C, ns > 1 ? scratch : nullptr, d, tr, kchunk);
+      check_launch("contract_dmma");
+    }
+  }
+  if (!dmma) {
+    k_contract<T><<<grid, 256, smem, st>>>(A, B, C, ns > 1 ? scratch : nullptr, d, tr, kchunk);
+    check_launch("contract");
+  }
   if (ns > 1) {
     const int64_t n = d.rows * d.cols;
     k_contract_reduce<T><<<(unsigned)((n + 31) / 32), 256, 0, st>>>(scratch, (int)ns, d, C);
