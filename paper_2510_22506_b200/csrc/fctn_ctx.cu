@@ -120,7 +120,9 @@ class Ctx : public Executor {
   double* partials = nullptr;
   int64_t partial_cap = 0;
   std::vector<double*> E64;               // E_j = A_(j)^T A_(j), the doubled-network nodes
-  double *epart = nullptr, *colstats = nullptr;
+  double *epart = nullptr, *colstats = nullptr;  // colstats: one [s x 3] slot per mode
+  int64_t cs_stride = 0;
+  double* colstats_of(int k) const { return colstats + cs_stride * k; }
   double* gnet[2] = {nullptr, nullptr};   // doubled-network intermediates
   std::vector<DftPlan> dft;
   std::vector<double*> mu, cosT, sinT;
@@ -135,7 +137,7 @@ class Ctx : public Executor {
   double* ework = nullptr;
   double* dft_gscr = nullptr;  // column work arrays of long-mode DFTs (I > 4266)
   cudaStream_t st2 = nullptr;
-  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_fork2 = nullptr, ev_side = nullptr;
   int solve_pref = 0;  // FCTN_SOLVE: 0 auto, 1 = "chol", 2 = "eigh", 3 = "tri"
   double *tri_d = nullptr, *tri_e = nullptr;  // T of the tridiagonal form
   enum { FORM_CHOL = 0, FORM_EIGH = 1, FORM_TRI = 2 };
@@ -457,9 +459,9 @@ class Ctx : public Executor {
     hstats = nullptr;
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
-    if (ev_fork) cudaEventDestroy(ev_fork);
-    if (ev_join) cudaEventDestroy(ev_join);
-    ev_fork = ev_join = nullptr;
+    for (cudaEvent_t e : {ev_fork, ev_join, ev_fork2, ev_side})
+      if (e) cudaEventDestroy(e);
+    ev_fork = ev_join = ev_fork2 = ev_side = nullptr;
     if (st2) cudaStreamDestroy(st2);
     st2 = nullptr;
     if (st) cudaStreamDestroy(st);
@@ -572,7 +574,8 @@ class Ctx : public Executor {
     CK(cudaMalloc(&ypart, max_yp * sizeof(double)));
     ypart_cap = max_yp;
     CK(cudaMalloc(&epart, max_ep * sizeof(double)));
-    CK(cudaMalloc(&colstats, max_s * 3 * sizeof(double)));
+    cs_stride = max_s * 3;
+    CK(cudaMalloc(&colstats, cs_stride * n * sizeof(double)));
     partial_cap = std::max<int64_t>(max_part, 4 * n_sm);
     CK(cudaMalloc(&partials, partial_cap * 4 * sizeof(double)));
     int64_t gcap = max_ss;
@@ -731,8 +734,8 @@ class Ctx : public Executor {
   void factor_refresh(int k) {
     const int64_t I = gsh.dims[k], S = gsh.s_of(k);
     const double sgn = sign == FCTN_SIGN_PD ? -1.0 : 1.0;
-    launch_factor_colstats(A64[k], I, S, delta[k], sgn, colstats, st);
-    launch_factor_gram(A64[k], I, S, epart, E64[k], colstats, dstats + 3 * k, st);
+    launch_factor_colstats(A64[k], I, S, delta[k], sgn, colstats_of(k), st);
+    launch_factor_gram(A64[k], I, S, epart, E64[k], colstats_of(k), dstats + 3 * k, st);
     launches += 3;
   }
 
@@ -785,6 +788,8 @@ class Ctx : public Executor {
     CK(cudaEventCreate(&ev1));
     CK(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&ev_fork2, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&ev_side, cudaEventDisableTiming));
     {
       const char* sv = getenv("FCTN_SOLVE");
       const std::string v = sv ? sv : "";
@@ -1200,17 +1205,21 @@ class Ctx : public Executor {
   void factor_update(int k, int zj, int extrap, double alpha, double beta) {
     const bool long_y = zj < 0 || zver[zj] != planner->versions[zj];
     const int form = form_for(k, long_y);
-    if (form != FORM_CHOL) {
-      // G_k and its decomposition need only the other factors' Grams: run
-      // them on the side stream while this stream forms Y_k
-      CK(cudaEventRecord(ev_fork, st));
-      CK(cudaStreamWaitEvent(st2, ev_fork, 0));
+    // G_k (and, for the eigh / tri forms, its decomposition) needs only the
+    // other factors' Grams E_j: the side stream forms it while this stream
+    // forms Y_k; the solve joins before it reads G
+    CK(cudaEventRecord(ev_fork, st));
+    CK(cudaStreamWaitEvent(st2, ev_fork, 0));
+    {
       const int64_t S = gsh.s_of(k);
       int pm = pbegin(FCTN_K_GRAM, st2);
       int64_t l0 = launches;
       gram_network(k, st2);
       pend(pm, 8.0 * S * S, launches - l0);
-      pm = pbegin(FCTN_K_EIGH, st2);
+    }
+    if (form != FORM_CHOL) {
+      const int64_t S = gsh.s_of(k);
+      int pm = pbegin(FCTN_K_EIGH, st2);
       if (form == FORM_EIGH) {
         launch_eigh(G, S, Vb[k], phi, ework, floor_shift[k], dstatus, 40, st2);
       } else {
@@ -1222,8 +1231,8 @@ class Ctx : public Executor {
       }
       ++launches;
       pend(pm, 8.0 * 3 * S * S, 1);
-      CK(cudaEventRecord(ev_join, st2));
     }
+    CK(cudaEventRecord(ev_join, st2));
     if (zj >= 0) {
       if (zver[zj] != planner->versions[zj]) compute_z(zj);
       y_from_z(zj, k);
@@ -1307,39 +1316,42 @@ class Ctx : public Executor {
         launch_rotate<double>(Ytmp, I, S, Vb[k], true, Ascratch, A64[k], extrap, alpha, beta, (double*)nullptr, st);
       else
         launch_rotate<float>(Ytmp, I, S, Vb[k], true, Ascratch, A64[k], extrap, alpha, beta, (float*)Ac[k], st);
-      launch_colstats3(Ascratch, A64[k], I, S, delta[k], sgn, colstats, st);
+      launch_colstats3(Ascratch, A64[k], I, S, delta[k], sgn, colstats_of(k), st);
       launches += 5;
       pend(pm, 8.0 * (6.0 * I * S + 4.0 * dp.H1 * S), 5);
     } else {
-    // G_k = M_k M_k^T by the doubled network (sylvester.py:57-59)
-    pm = pbegin(FCTN_K_GRAM);
-    int64_t l0 = launches;
-    gram_network(k, st);
-    pend(pm, 8.0 * S * S, launches - l0);
+    // G_k = M_k M_k^T by the doubled network (sylvester.py:57-59) came from
+    // the side stream (factor_update)
     // K3: DFT along mode k, per-frequency SPD solves, inverse DFT (sylvester.py:108-116)
     pm = pbegin(FCTN_K_DFT);
     launch_dft_fwd(Y, dp, S, cosT[k], sinT[k], Fr, Fi, st, dft_gscr);
     pend(pm, 8.0 * (I * S + 2.0 * dp.H1 * S), 1);
+    CK(cudaStreamWaitEvent(st, ev_join, 0));
     pm = pbegin(FCTN_K_SOLVE);
     launch_chol_solve(G, S, dp.H1, mu[k], Fr, Fi, check_mu[k], dstatus, st);
     pend(pm, 8.0 * (S * S + 4.0 * dp.H1 * S), 1);
     pm = pbegin(FCTN_K_DFT);
     const int ninv = dtype == FCTN_F64
                          ? launch_dft_inv<double>(Fr, Fi, dp, S, cosT[k], sinT[k], A64[k], Ascratch, nullptr, extrap,
-                                                  alpha, beta, delta[k], sgn, colstats, st, nullptr, nullptr,
+                                                  alpha, beta, delta[k], sgn, colstats_of(k), st, nullptr, nullptr,
                                                   dft_gscr)
                          : launch_dft_inv<float>(Fr, Fi, dp, S, cosT[k], sinT[k], A64[k], Ascratch, (float*)Ac[k],
-                                                 extrap, alpha, beta, delta[k], sgn, colstats, st, nullptr, nullptr,
+                                                 extrap, alpha, beta, delta[k], sgn, colstats_of(k), st, nullptr, nullptr,
                                                  dft_gscr);
     launches += ninv - 1;
     pend(pm, 8.0 * (3.0 * I * S + 2.0 * dp.H1 * S), ninv);
     }
-    pm = pbegin(FCTN_K_FGRAM);
-    launch_factor_gram(Ascratch, I, S, epart, E64[k], colstats, dstats + 3 * k, st);
-    pend(pm, 8.0 * (I * S + S * S), 2);
     if (mbuf_holds >= 0 && mbuf_holds != k) mbuf_holds = -1;  // M_j (j != k) contains A_k
     // keep every factor at a fixed address (the sweep may be replayed as a CUDA graph)
     CK(cudaMemcpyAsync(A64[k], Ascratch, I * S * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    // E_k = A_(k)^T A_(k) and the factor statistics are needed only by the
+    // next update's Gram network (side stream) and the sweep's final stats:
+    // off the critical path
+    CK(cudaEventRecord(ev_fork2, st));
+    CK(cudaStreamWaitEvent(st2, ev_fork2, 0));
+    pm = pbegin(FCTN_K_FGRAM, st2);
+    launch_factor_gram(A64[k], I, S, epart, E64[k], colstats_of(k), dstats + 3 * k, st2);
+    pend(pm, 8.0 * (I * S + S * S), 2);
     launches += 7;
     planner->versions[k] += 1;  // network.py:200
     if (k == 0) refresh_slab();
@@ -1452,6 +1464,10 @@ class Ctx : public Executor {
       planner->meter.compose += planner->compose_chain_flops();
       compose(n - 1, false);
     }
+    // rejoin the side stream (the last E_k / factor statistics) before the
+    // sweep's scalars are read; also closes the fork for graph capture
+    CK(cudaEventRecord(ev_side, st2));
+    CK(cudaStreamWaitEvent(st, ev_side, 0));
   }
 
   static std::string graph_key(const std::vector<int>& order, int cur_, int extrap, double alpha, double beta) {
