@@ -189,6 +189,7 @@ class Ctx : public Executor {
   bool zroute = true;    // FCTN_NO_ZROUTE=1 disables
   // Y_k without M_k (alt_join): armed per update by sweep_device
   bool alt_route = true;  // FCTN_NO_ALTJOIN=1 disables
+  bool force_assoc = false;  // FCTN_FORCE_ASSOC=1 (tests): take the other associations whenever they apply
   bool alt_ok = false;
   int alt_k = -1;
   bool y_ready = false;
@@ -779,6 +780,8 @@ class Ctx : public Executor {
       zroute = !(zr && zr[0] == '1');
       const char* aj = getenv("FCTN_NO_ALTJOIN");
       alt_route = !(aj && aj[0] == '1');
+      const char* fa = getenv("FCTN_FORCE_ASSOC");
+      force_assoc = fa && fa[0] == '1';
       const char* t = getenv("FCTN_TF32");
       split3 = !(t && std::string(t) == "1x");
     }
@@ -1069,7 +1072,7 @@ class Ctx : public Executor {
                          8.0 * (T + rn + 2.0 * wr + ln) / Bw;
     const bool first_left = alt_l <= alt_r;
     const double w_numel = first_left ? wl : wr;
-    if (std::min(alt_l, alt_r) > 0.5 * cur) return false;  // only when clearly cheaper
+    if (std::min(alt_l, alt_r) > 0.5 * cur && !force_assoc) return false;  // only when clearly cheaper
     const LTensor& first = first_left ? left : right;
     const LTensor& second = first_left ? right : left;
     int pm = pbegin(FCTN_K_STREAM_Y);
@@ -1183,7 +1186,7 @@ class Ctx : public Executor {
     const double b = (double)esize, F = dtype == FCTN_F32 ? 75e12 : 10e12, B = 5e12;
     const double cur = 2.0 * mn * kjoin / F + b * mn / B;
     const double alt = (2.0 * numel(t1) * k1 + 2.0 * mn * k2) / F + b * (2.0 * numel(t1) + mn) / B;
-    if (alt > 0.8 * cur || numel(t1) > 0.5 * mn) return false;
+    if ((alt > 0.8 * cur || numel(t1) > 0.5 * mn) && !force_assoc) return false;
     ContractOp op1;
     op1.a = base;
     op1.b.labels = sh.factor_labels(first);

@@ -238,3 +238,29 @@ def test_gpu_general_sizes_match_oracle(dims, rank, iters):
         assert rel(res.factors.factor(k), ref.factors[k]) <= FP64_TOL, k
     for a, b in zip(res.trace, ref.trace):
         assert a.objective == pytest.approx(b.objective, rel=FP64_TOL)
+
+
+@pytest.mark.parametrize("dtype", ["float64", "float32"])
+@pytest.mark.parametrize("name", ["n4_afctnlr_shuffle", "n4_afctnlr_identity", "n5_afctnlr", "n5_budget_binds",
+                                  "n4_nonuniform_rank"])
+def test_gpu_other_associations_match_reference(monkeypatch, name, dtype):
+    """The device's own contraction orders, forced wherever they apply
+    (FCTN_FORCE_ASSOC=1): Y_k = (X (*) F) (*) F' without M_k (alt_join, FP64)
+    and the final join reassociated one factor at a time (reassoc_join) —
+    against the reference's goldens (FP64: 1e-9; FP32: its bound), with the
+    trace integers still the reference's."""
+    monkeypatch.setenv("FCTN_FORCE_ASSOC", "1")
+    case = load_run(name)
+    res = P.run(P.Observation(case["values"], case["mask"]), _cfg(case["config"]), dtype=dtype)
+    tol = FP64_TOL if dtype == "float64" else 2e-4
+    if dtype == "float32":
+        ref = O.run(case["values"].astype(np.float32).astype(np.float64), case["mask"],
+                    **{k: v for k, v in case["config"].items()})
+        assert rel(res.x, ref.x) <= tol
+    else:
+        assert rel(res.x, case["x"]) <= tol
+        for k, f in enumerate(case["factors"]):
+            assert rel(res.factors.factor(k), f) <= tol, k
+    for i, r in enumerate(res.trace):
+        assert (r.flops, r.mk_flops, r.cache_hits) == (case["trace_flops"][i], case["trace_mk_flops"][i],
+                                                      case["trace_cache_hits"][i])
