@@ -5,6 +5,7 @@
 // partial sums.  M_k is p-fastest (M[p + pk s]).
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <stdexcept>
 #include <string>
 
@@ -160,6 +161,48 @@ __global__ void __launch_bounds__(1024) k_reduce4(const double* __restrict__ par
     __syncthreads();
   }
   if (tid < 4) out[tid] = red[tid][0];
+}
+
+// The P_Omega blend of an already formed C (compose through the partials,
+// fctn_ctx.cu compose_via_partials): X_new = Omega ? X_old : (rho X_old + C) /
+// (1 + rho) in the reference's rounding, and the same four per-block sums as
+// k_compose (solver.py:220,227-237,346-354,382).
+__global__ void __launch_bounds__(256) k_blend(const double* __restrict__ C, const double* __restrict__ Xo,
+                                               const uint8_t* __restrict__ mask, double* __restrict__ Xn,
+                                               int64_t T, double r, double* __restrict__ partials) {
+  __shared__ double red[4][256];
+  const int tid = threadIdx.x;
+  const double onep = 1.0 + r;
+  double s_d = 0.0, s_b = 0.0, s_c = 0.0, s_n = 0.0;
+  for (int64_t e = blockIdx.x * 256LL + tid; e < T; e += (int64_t)gridDim.x * 256) {
+    const double x = Xo[e], c = C[e];
+    const double xn = mask[e] ? x : div_rn(add_rn(mul_rn(x, r), c), onep);
+    Xn[e] = xn;
+    const double dx = xn - x, dc = xn - c;
+    s_d += dx * dx;
+    s_b += x * x;
+    s_c += dc * dc;
+    s_n += xn * xn;
+  }
+  red[0][tid] = s_d;
+  red[1][tid] = s_b;
+  red[2][tid] = s_c;
+  red[3][tid] = s_n;
+  __syncthreads();
+  for (int off = 128; off > 0; off >>= 1) {
+    if (tid < off)
+      for (int q = 0; q < 4; ++q) red[q][tid] += red[q][tid + off];
+    __syncthreads();
+  }
+  if (tid < 4) partials[blockIdx.x * 4 + tid] = red[tid][0];
+}
+
+int launch_blend(const double* C, const double* Xo, const uint8_t* mask, double* Xn, int64_t T, double rho,
+                 double* partials, int64_t partial_cap, cudaStream_t st) {
+  const int64_t blocks = std::min<int64_t>(std::min<int64_t>((T + 255) / 256, 148 * 8), partial_cap);
+  k_blend<<<(unsigned)blocks, 256, 0, st>>>(C, Xo, mask, Xn, T, rho, partials);
+  check_launch("blend");
+  return (int)blocks;
 }
 
 void launch_reduce4(const double* partials, int64_t n, double* out, cudaStream_t st) {

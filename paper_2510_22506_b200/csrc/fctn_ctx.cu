@@ -192,7 +192,14 @@ class Ctx : public Executor {
   bool force_assoc = false;  // FCTN_FORCE_ASSOC=1 (tests): take the other associations whenever they apply
   bool alt_ok = false;
   int alt_k = -1;
+  bool alt_last = false;  // alt_k is the order's last mode: the compose needs M_k or the partials
+  bool assoc_ok = false;  // set around the sweep's M_k builds only (the hooks read alt_k)
   bool y_ready = false;
+  // compose through the partials (compose_via_partials): the last update's
+  // left / right partials are kept alive until the compose
+  bool compose_alt = false;
+  LTensor cp_left, cp_right;
+  std::vector<int64_t> held_bufs, held_frees;
   // Three-mode sweeps have no data-dependent host decisions and no allocations,
   // so each (visiting order, X buffer parity, extrapolation) sweep is captured
   // once as a CUDA graph and replayed (FCTN_NO_GRAPH=1 disables).
@@ -276,6 +283,10 @@ class Ctx : public Executor {
   }
   void free(int64_t id) override {
     if (id == M_ID) return;
+    if (std::find(held_bufs.begin(), held_bufs.end(), id) != held_bufs.end()) {  // kept for the compose
+      held_frees.push_back(id);
+      return;
+    }
     auto it = bufs.find(id);
     if (it == bufs.end()) return;
     CK(cudaFreeAsync(it->second, st));
@@ -1035,7 +1046,7 @@ class Ctx : public Executor {
   // the compose reads M_last) on the FP64, unsharded path; the FLOP meter
   // still records the reference's join (plan.cpp).
   bool alt_join(const LTensor& left, const LTensor& right) {
-    if (!alt_ok || !alt_route) return false;
+    if (!assoc_ok || !alt_ok || !alt_route) return false;
     const int k = alt_k;
     const int n = sh.n;
     const int64_t T = sh.total(), I = sh.dims[k], S = sh.s_of(k);
@@ -1072,7 +1083,20 @@ class Ctx : public Executor {
                          8.0 * (T + rn + 2.0 * wr + ln) / Bw;
     const bool first_left = alt_l <= alt_r;
     const double w_numel = first_left ? wl : wr;
-    if (std::min(alt_l, alt_r) > 0.5 * cur && !force_assoc) return false;  // only when clearly cheaper
+    double alt_cost = std::min(alt_l, alt_r), cur_cost = cur;
+    if (alt_last) {
+      // the compose then also runs through the partials (compose_via_partials)
+      // instead of reading M_k: C = (A_k (*) F) (*) F'
+      const double vl = (double)I * (double)(S / sl) * (ln / (double)sl);  // A_k (*) left
+      const double vr = (double)I * (double)(S / sr) * (rn / (double)sr);  // A_k (*) right
+      const double c_l = (2.0 * (double)I * S * (ln / sl) + 2.0 * (double)T * (double)(S / sl) * rsz) / Fr_ +
+                         8.0 * (2.0 * vl + rn + 2.0 * T) / Bw;
+      const double c_r = (2.0 * (double)I * S * (rn / sr) + 2.0 * (double)T * (double)(S / sr) * rsz) / Fr_ +
+                         8.0 * (2.0 * vr + ln + 2.0 * T) / Bw;
+      alt_cost += std::min(c_l, c_r);
+      cur_cost += 2.0 * (double)T * S / Fr_ + 8.0 * (m_numel + 2.0 * T) / Bw;
+    }
+    if (alt_cost > 0.5 * cur_cost && !force_assoc) return false;  // only when clearly cheaper
     const LTensor& first = first_left ? left : right;
     const LTensor& second = first_left ? right : left;
     int pm = pbegin(FCTN_K_STREAM_Y);
@@ -1129,7 +1153,78 @@ class Ctx : public Executor {
     ++launches;
     pend(pm, 8.0 * (T + w_numel * 2 + ln + rn + 2.0 * I * S), 4);
     y_ready = true;
+    if (alt_last) {  // keep both partials for the compose
+      cp_left = left;
+      cp_right = right;
+      held_bufs.clear();
+      for (const LTensor* t : {&left, &right})
+        if (t->factor < 0 && t->buf >= 0) held_bufs.push_back(t->buf);
+      compose_alt = true;
+    }
     return true;
+  }
+
+  // C = A_k (*) M_k as (A_k (*) F) (*) F' from the last update's partials, then
+  // the P_Omega blend and sums (solver.py:227-237,346-354): no M_k at all.
+  void compose_via_partials(int k) {
+    const int n = sh.n;
+    const int64_t T = sh.total();
+    auto has = [](const std::vector<int>& v, int l) { return std::find(v.begin(), v.end(), l) != v.end(); };
+    auto out_of = [&](const std::vector<int>& a, const std::vector<int>& b) {
+      std::vector<int> o;
+      for (int l : a)
+        if (!has(b, l)) o.push_back(l);
+      for (int l : b)
+        if (!has(a, l)) o.push_back(l);
+      std::sort(o.begin(), o.end());
+      return o;
+    };
+    auto numel = [&](const std::vector<int>& ls) {
+      double e = 1;
+      for (int l : ls) e *= (double)sh.extent(l);
+      return e;
+    };
+    LTensor ak;
+    ak.labels = sh.factor_labels(k);
+    ak.factor = k;
+    // absorb the side giving the smaller intermediate first
+    const std::vector<int> vl = out_of(ak.labels, cp_left.labels), vr = out_of(ak.labels, cp_right.labels);
+    const bool left_first = numel(vl) <= numel(vr);
+    const LTensor& f1 = left_first ? cp_left : cp_right;
+    const LTensor& f2 = left_first ? cp_right : cp_left;
+    int pm = pbegin(FCTN_K_COMPOSE);
+    ContractOp op1;
+    op1.a = ak;
+    op1.b = f1;
+    op1.out.labels = left_first ? vl : vr;
+    op1.out.buf = alloc_labels(op1.out.labels);
+    contract(op1);
+    ContractOp op2;
+    op2.a = op1.out;
+    op2.b = f2;
+    op2.out.labels.resize(n);
+    for (int j = 0; j < n; ++j) op2.out.labels[j] = j;  // X's own layout
+    op2.out.buf = alloc_labels(op2.out.labels);
+    {
+      bool sw = false;
+      ContractDesc d = desc_for(op2, &sw);
+      launch_contract<double>((const double*)ptr_of(sw ? op2.b : op2.a), (const double*)ptr_of(sw ? op2.a : op2.b),
+                              (double*)ptr_of(op2.out), d, cscratch, cscratch_cap, n_sm, st);
+      ++launches;
+    }
+    free(op1.out.buf);
+    const int nb = launch_blend((const double*)ptr_of(op2.out), (const double*)X[cur], mask, (double*)X[cur ^ 1], T,
+                                rho, partials, partial_cap, st);
+    launch_reduce4(partials, nb, dstats + 3 * sh.n, st);
+    allreduce_sum(dstats + 3 * sh.n, 4);
+    launches += 2;
+    free(op2.out.buf);
+    pend(pm, 8.0 * (3.0 * T + numel(op1.out.labels) * 2.0 + (double)f1.numel(sh) + (double)f2.numel(sh)) + (double)T,
+         4);
+    compose_alt = false;
+    held_bufs.clear();
+    for (int64_t id : held_frees) free(id);
+    held_frees.clear();
   }
 
   // M_k in another association.  The reference's final join contracts two
@@ -1141,7 +1236,7 @@ class Ctx : public Executor {
   // (tensor-core FLOPs at the 3xTF32 rate, bytes at HBM rate).
   bool reassoc_join(const LTensor& left, const LTensor& right, const std::vector<int>& lseq,
                     const std::vector<int>& rseq) {
-    if (!alt_route || sharded()) return false;
+    if (!assoc_ok || !alt_route || sharded()) return false;
     const bool absorb_right = rseq.size() <= lseq.size();
     const std::vector<int>& fs = absorb_right ? rseq : lseq;
     if (fs.size() != 2) return false;
@@ -1428,6 +1523,9 @@ class Ctx : public Executor {
   void sweep_device(const std::vector<int>& order, int extrap, double alpha, double beta) {
     const int n = sh.n;
     const std::vector<int> route = plan_routes(order);
+    compose_alt = false;
+    held_bufs.clear();
+    held_frees.clear();
     bool side = false;
     for (int k = 0; k < n; ++k) side |= form_for(k, true) != FORM_CHOL;
     tc_reserve_sms(side ? 1 : 0);  // one SM for the concurrent eigendecomposition
@@ -1436,18 +1534,24 @@ class Ctx : public Executor {
       const bool zr = route[t] >= 0;
       y_ready = false;
       alt_k = k;
-      alt_ok = dtype == FCTN_F64 && !sharded() && n >= 4 && k != order.back();
+      alt_ok = dtype == FCTN_F64 && !sharded() && n >= 4 && alg == FCTN_ALG_ACCEL;
+      alt_last = k == order.back();
+      assoc_ok = true;
       if (alg == FCTN_ALG_ACCEL) {
         planner->partial_cached(k, order, zr ? nullptr : this, M_ID);  // dry replay when M_k is not needed
       } else {
         planner->partial_plain(k, zr ? nullptr : this, M_ID);
       }
       alt_ok = false;
+      assoc_ok = false;
       mbuf_holds = (zr || y_ready) ? -1 : k;
       factor_update(k, route[t], extrap, alpha, beta);
     }
     int k_last = order.back();
-    if (alg == FCTN_ALG_ACCEL) {
+    if (alg == FCTN_ALG_ACCEL && compose_alt) {
+      planner->meter.compose += 2 * (gsh.total() / gsh.dims[k_last]) * gsh.s_of(k_last) * gsh.dims[k_last];
+      compose_via_partials(k_last);
+    } else if (alg == FCTN_ALG_ACCEL) {
       planner->meter.compose += 2 * (gsh.total() / gsh.dims[k_last]) * gsh.s_of(k_last) * gsh.dims[k_last];
       int kc = k_last;
       if (sh.n == 3 && zroute) {

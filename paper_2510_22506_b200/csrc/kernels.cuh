@@ -189,6 +189,9 @@ void launch_tf32_split(const float* x, float* hi, float* lo, int64_t n, cudaStre
 void launch_pack_mask(const uint8_t* mask, int64_t T, uint32_t* bits, cudaStream_t st);
 // fixed-order final reduction of n x 4 partials into out[0..3]
 void launch_reduce4(const double* partials, int64_t n, double* out, cudaStream_t st);
+// the blend + sums of K4 for an already formed C (T entries, fp64)
+int launch_blend(const double* C, const double* Xo, const uint8_t* mask, double* Xn, int64_t T, double rho,
+                 double* partials, int64_t partial_cap, cudaStream_t st);
 
 // ---------------------------------------------------------------- quality metrics (metrics.cu)
 // psnr / ssim / rel_err of metrics.py:33-105 over F-order slices of hw entries

@@ -172,19 +172,27 @@ LTensor Planner::chain(const std::vector<int>& seq, bool from_right, Executor* e
     std::vector<int> mlab;
     if (to_m) mlab = sh_.m_labels(k);
     LTensor nxt;
-    if (from_right) {
-      int j = steps[idx].front();
-      LTensor f;
-      f.labels = sh_.factor_labels(j);
-      f.factor = j;
-      nxt = contract(f, arr, exec, to_m ? &mlab : nullptr, to_m ? m_buf : -1, tag_compose);
-    } else {
-      int j = steps[idx].back();
-      LTensor f;
-      f.labels = sh_.factor_labels(j);
-      f.factor = j;
-      nxt = contract(arr, f, exec, to_m ? &mlab : nullptr, to_m ? m_buf : -1, tag_compose);
+    const int j = from_right ? steps[idx].front() : steps[idx].back();
+    LTensor f;
+    f.labels = sh_.factor_labels(j);
+    f.factor = j;
+    const LTensor& lt = from_right ? f : arr;
+    const LTensor& rt = from_right ? arr : f;
+    // the step that produces M_k is the final join of this side: the device
+    // may form it (or Y_k) in another association (final_join_hook)
+    bool hooked = false;
+    if (to_m && exec && final_join_hook && !tag_compose) {
+      std::vector<int> lfs(steps[idx].begin(), steps[idx].end()), rfs;
+      if (from_right) {
+        rfs.assign(steps[idx].begin() + 1, steps[idx].end());
+        lfs.assign(1, j);
+      } else {
+        lfs.assign(steps[idx].begin(), steps[idx].end() - 1);
+        rfs.assign(1, j);
+      }
+      hooked = final_join_hook(lt, rt, lfs, rfs);
     }
+    nxt = contract(lt, rt, hooked ? nullptr : exec, to_m ? &mlab : nullptr, to_m ? m_buf : -1, tag_compose);
     release(arr, exec);
     arr = nxt;
     if (to_m && produced_m) *produced_m = true;
