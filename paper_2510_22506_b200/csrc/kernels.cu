@@ -517,7 +517,7 @@ void launch_contract(const T* A, const T* B, T* C, const ContractDesc& d, T* scr
   // what the specialised forms above do not take: FP64 on the tensor cores
   // (measured faster than the SIMT tile, slower than k_join on the joins)
   static const bool no_dmma = getenv("FCTN_NO_DMMA") != nullptr;
-  const bool dmma = std::is_same<T, double>::value && !no_dmma && d.rows >= 16 && d.cols >= 16 && d.K >= 4;
+  const bool dmma = std::is_same<T, double>::value && !no_dmma && d.K >= 4;
   int64_t ns = 1;
   if (scratch && tiles < n_sm && d.K >= 256) {
     ns = std::min<int64_t>(d.K / 64, (2 * n_sm + tiles - 1) / tiles);
