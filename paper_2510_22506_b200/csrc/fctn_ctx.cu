@@ -1847,6 +1847,7 @@ struct Stager {
     }
     const unsigned hc = std::thread::hardware_concurrency();
     nthr = (int)std::max(1u, std::min(8u, hc ? hc / 2 : 1u));
+    if (const char* e = getenv("FCTN_STAGE_THREADS")) nthr = std::max(1, atoi(e));
   }
   ~Stager() {
     for (int b = 0; b < NB; ++b) {
