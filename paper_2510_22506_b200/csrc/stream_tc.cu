@@ -548,27 +548,32 @@ __global__ void __launch_bounds__(TS_THREADS, 1)
 
 // Persistent form of k_stream_ts for unsplit products with many row tiles
 // (the Z_j passes): one CTA per SM walks its row tiles with one continuous
-// operand pipeline; two TMEM accumulators let four epilogue warps drain tile
-// j while the MMA already accumulates tile j + 1.
+// operand pipeline.  NACC = 1 (default): one TMEM accumulator, which leaves
+// TMEM for a 6-stage operand ring instead of 4 (NT = 64); the epilogue warps
+// pull a finished tile's rows into registers, hand the accumulator straight
+// back to the MMA and only then store, so the MMA stalls for a TMEM read per
+// tile (~1 us of 30) while the ring keeps filling.  Measured at c4: 230 ->
+// 217 us per Z pass.  NACC = 2 (FCTN_ZPASS_ACC2=1): two accumulators, the
+// epilogue of tile j overlaps the MMAs of tile j + 1, 4 stages.
 constexpr int TSP_EPI_WARPS = 4;
 constexpr int TSP_THREADS = 64 + 32 * (TS_CONV_WARPS + TSP_EPI_WARPS);
-template <int NT>
+template <int NT, int NACC>
 struct TspSmem {
   static constexpr int B_BYTES = NT * BK * 4;
   static constexpr int STAGE_BYTES = A_BYTES + 2 * B_BYTES;
   static constexpr int ACC = 2 * NT;  // one accumulator: [hi x (B hi | B lo)]
   static constexpr int S_SMEM = (200 * 1024) / STAGE_BYTES > 6 ? 6 : (200 * 1024) / STAGE_BYTES;
-  static constexpr int S_TMEM = (512 - 2 * ACC) / 64;
+  static constexpr int S_TMEM = (512 - NACC * ACC) / 64;
   static constexpr int STAGES = S_SMEM < S_TMEM ? S_SMEM : S_TMEM;
   static constexpr int TOTAL = STAGES * STAGE_BYTES + 1024 + 256;
 };
 
-template <int NT, bool AMN>
+template <int NT, bool AMN, int NACC>
 __global__ void __launch_bounds__(TSP_THREADS, 1)
     k_stream_tsp(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmM,
                  const __grid_constant__ CUtensorMap tmMl, float* __restrict__ out, int I, int S, int nkb,
                  int n_tiles, int nPB, int b_pre, int x3d, int rows_b) {
-  using L = TspSmem<NT>;
+  using L = TspSmem<NT, NACC>;
   constexpr int STAGES = L::STAGES;
   static_assert(STAGES >= 2, "stage ring");
   extern __shared__ uint8_t smem_raw[];
@@ -591,7 +596,7 @@ __global__ void __launch_bounds__(TSP_THREADS, 1)
       tc::mbar_init(&conv[s], TS_CONV_WARPS);
       tc::mbar_init(&empty[s], 1);
     }
-    for (int a = 0; a < 2; ++a) {
+    for (int a = 0; a < NACC; ++a) {
       tc::mbar_init(&tfull[a], 1);
       tc::mbar_init(&tempty[a], TSP_EPI_WARPS);
     }
@@ -642,8 +647,8 @@ __global__ void __launch_bounds__(TSP_THREADS, 1)
     constexpr uint32_t idesc1 = tc::idesc_tf32(128, NT, false, false);
     int g = 0, j = 0;
     for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++j) {
-      const int acc = j & 1;
-      tc::mbar_wait(&tempty[acc], ((j >> 1) & 1) ^ 1);
+      const int acc = j % NACC;
+      tc::mbar_wait(&tempty[acc], ((j / NACC) & 1) ^ 1);
       tc::fence_after_sync();
       const uint32_t d = tmem + acc * L::ACC;
       for (int kb = 0; kb < nkb; ++kb, ++g) {
@@ -651,7 +656,7 @@ __global__ void __launch_bounds__(TSP_THREADS, 1)
         tc::mbar_wait(&conv[s], (g / STAGES) & 1);
         tc::fence_after_sync();
         const uint32_t b = tc::smem_u32(smem + s * L::STAGE_BYTES) + A_BYTES;
-        const uint32_t ahi = tmem + 2 * L::ACC + 64 * s, alo = ahi + 32;
+        const uint32_t ahi = tmem + NACC * L::ACC + 64 * s, alo = ahi + 32;
 #pragma unroll
         for (int kk = 0; kk < BK / 8; ++kk) {
           const uint64_t bd = tc::sdesc(b + kk * 32, 16, 1024);
@@ -701,7 +706,7 @@ __global__ void __launch_bounds__(TSP_THREADS, 1)
           lo[jj] = tc::tf32_rn_int(x[jj] - h);
           x[jj] = h;
         }
-        const uint32_t ta = tmem + ((uint32_t)(32 * q) << 16) + 2 * L::ACC + 64 * s + 16 * hf;
+        const uint32_t ta = tmem + ((uint32_t)(32 * q) << 16) + NACC * L::ACC + 64 * s + 16 * hf;
         tc::tmem_st16(ta, x);
         tc::tmem_st16(ta + 32, lo);
         if (!b_pre) {
@@ -721,11 +726,33 @@ __global__ void __launch_bounds__(TSP_THREADS, 1)
     const int row = 32 * q + lane;
     int j = 0;
     for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++j) {
-      const int acc = j & 1;
-      tc::mbar_wait(&tfull[acc], (j >> 1) & 1);
+      const int acc = j % NACC;
+      tc::mbar_wait(&tfull[acc], (j / NACC) & 1);
       tc::fence_after_sync();
       const long long i = (long long)t * 128 + row;
       const uint32_t base = tmem + ((uint32_t)(32 * q) << 16) + acc * L::ACC;
+      if (NACC == 1) {
+        // one accumulator: pull the whole row into registers, hand the
+        // accumulator back to the MMA, then store
+        float v[NT];
+#pragma unroll
+        for (int c0 = 0; c0 < NT; c0 += 16) {
+          float w[16];
+          tc::tmem_ld16(base + c0, v + c0);
+          tc::tmem_ld16(base + NT + c0, w);
+#pragma unroll
+          for (int jj = 0; jj < 16; ++jj) v[c0 + jj] += w[jj];
+        }
+        tc::fence_before_sync();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(&tempty[acc]);
+        if (i < I) {
+#pragma unroll
+          for (int sc = 0; sc < NT; ++sc)
+            if (sc < S) out[i + (long long)I * sc] = v[sc];
+        }
+        continue;
+      }
 #pragma unroll 1
       for (int c0 = 0; c0 < NT; c0 += 16) {
         float v[16], w[16];
@@ -811,8 +838,9 @@ void go_ts(const CUtensorMap& mx, const CUtensorMap& mm, const CUtensorMap& mml,
   static const bool no_persist = getenv("FCTN_STREAM_NO_PERSIST") != nullptr;
   if constexpr (NT <= 64) {
     if (tp.nsplit == 1 && tp.n_mtiles > sm_count() && !no_persist && tp.nkb < (1LL << 31)) {
-      const int smem = TspSmem<NT>::TOTAL;
-      auto fn = k_stream_tsp<NT, AMN>;
+      static const bool acc2 = getenv("FCTN_ZPASS_ACC2") != nullptr;  // the older double-buffered accumulator
+      const int smem = acc2 ? TspSmem<NT, 2>::TOTAL : TspSmem<NT, 1>::TOTAL;
+      auto fn = acc2 ? k_stream_tsp<NT, AMN, 2> : k_stream_tsp<NT, AMN, 1>;
       cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
       if (e != cudaSuccess) throw std::runtime_error(std::string("stream_tsp smem: ") + cudaGetErrorString(e));
       const int grid = (int)std::min<int64_t>(tp.n_mtiles, std::max(1, sm_count() - g_reserved_sms));
