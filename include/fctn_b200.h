@@ -142,6 +142,14 @@ typedef int (*fctn_host_allgather_fn)(void* user, const double* send, double* re
 int fctn_set_comm_host(fctn_ctx* ctx, fctn_host_allreduce_fn allreduce, fctn_host_allgather_fn allgather,
                        void* user, int rank, int nranks, int64_t slab_lo, int64_t slab_hi);
 
+/* Per-rank timing model and tests only: the same sharding with device-side
+ * loop-back collectives (all-reduce = this rank's own part, all-gather =
+ * nranks copies of the local block).  The results are not the global ones;
+ * every kernel has the shape it has on a real nranks-GPU run and the sweep is
+ * captured and replayed as a CUDA graph exactly as with NCCL, so one GPU can
+ * time what a rank does between its collectives. */
+int fctn_set_comm_loopback(fctn_ctx* ctx, int rank, int nranks, int64_t slab_lo, int64_t slab_hi);
+
 /* Kernel self-test (tests only): Y = X_(k) M^T for a mode-k view X of
  * extents [P, I, Q] (first fastest) and a p-fastest M (p = P*Q, S rows),
  * through the K2 path the context would use (tcgen05 TF32 when use_tc and

@@ -23,7 +23,7 @@ CT_FLOPS, CT_MK, CT_COMPOSE, CT_HITS, CT_LAUNCHES, CT_COUNT = 0, 1, 2, 3, 4, 8
 
 EXPORTS = [
     "fctn_create", "fctn_upload", "fctn_upload_f64", "fctn_get_x_f64", "fctn_set_factors", "fctn_set_rank", "fctn_get_factors", "fctn_get_x",
-    "fctn_objective", "fctn_sweep", "fctn_plan_sweeps", "fctn_nccl_unique_id", "fctn_set_comm", "fctn_set_comm_host",
+    "fctn_objective", "fctn_sweep", "fctn_plan_sweeps", "fctn_nccl_unique_id", "fctn_set_comm", "fctn_set_comm_host", "fctn_set_comm_loopback",
     "fctn_sync", "fctn_selftest_stream", "fctn_selftest_chol", "fctn_selftest_eigh", "fctn_timer", "fctn_set_profiling", "fctn_get_profile", "fctn_last_error", "fctn_version",
     "fctn_quality", "fctn_quality_ctx", "fctn_destroy",
 ]
@@ -96,6 +96,7 @@ def lib():
     L.fctn_nccl_unique_id.argtypes = [P]
     L.fctn_set_comm.argtypes = [P, P, C.c_int, C.c_int, C.c_int64, C.c_int64]
     L.fctn_set_comm_host.argtypes = [P, HOST_ALLREDUCE, HOST_ALLGATHER, P, C.c_int, C.c_int, C.c_int64, C.c_int64]
+    L.fctn_set_comm_loopback.argtypes = [P, C.c_int, C.c_int, C.c_int64, C.c_int64]
     L.fctn_sync.argtypes = [P]
     L.fctn_selftest_chol.argtypes = [C.c_int, C.c_int64, C.c_int64, P, P, P, P, C.c_int, f64p]
     L.fctn_selftest_eigh.argtypes = [C.c_int, C.c_int64, P, P, P, C.c_int, f64p, C.POINTER(C.c_int)]
@@ -343,6 +344,13 @@ class Context:
         lo, hi = slab_of(self.dims[0], rank, nranks)
         buf = (C.c_uint8 * 128).from_buffer_copy(uid)
         self._check(lib().fctn_set_comm(self.h, buf, rank, nranks, lo, hi))
+        self._set_slab(lo, hi)
+
+    def set_comm_loopback(self, rank: int, nranks: int):
+        """Device-side loop-back collectives (timing model / tests): this rank's
+        slab with every kernel at its nranks-GPU shape, sweeps graph-replayed."""
+        lo, hi = slab_of(self.dims[0], rank, nranks)
+        self._check(lib().fctn_set_comm_loopback(self.h, rank, nranks, lo, hi))
         self._set_slab(lo, hi)
 
     def set_comm_host(self, allreduce, allgather, rank: int, nranks: int):

@@ -626,6 +626,7 @@ class Ctx : public Executor {
   }
   void allreduce_sum(double* d, int64_t n) {
     if (nranks == 1 && comm.kind == 0) return;
+    if (comm.kind == 3) return;  // loop-back: the sum over ranks is this rank's own part
     if (comm.kind == 1) {
       if (comm.allreduce(d, d, (size_t)n, ncclFloat64, ncclSum, (ncclComm_t)comm.nccl, st) != ncclSuccess)
         throw std::runtime_error("ncclAllReduce failed");
@@ -649,6 +650,9 @@ class Ctx : public Executor {
       if (comm.h_allgather(comm.user, comm.hbuf, comm.hbuf + n, n) != 0)
         throw std::runtime_error("host allgather callback failed");
       CK(cudaMemcpyAsync(recv, comm.hbuf + n, n * nranks * sizeof(double), cudaMemcpyHostToDevice, st));
+    } else if (comm.kind == 3) {
+      for (int r = 0; r < nranks; ++r)  // loop-back: every rank's block is this rank's
+        CK(cudaMemcpyAsync(recv + (int64_t)r * n, send, n * sizeof(double), cudaMemcpyDeviceToDevice, st));
     } else {
       CK(cudaMemcpyAsync(recv, send, n * sizeof(double), cudaMemcpyDeviceToDevice, st));
     }
@@ -1658,7 +1662,9 @@ class Ctx : public Executor {
     Meter m0 = planner->meter;
     int64_t hits0 = planner->cache().hits;
     launches = 0;
-    const bool graphable = use_graph && sh.n == 3 && !prof && comm.kind == 0 && !sharded();
+    // NCCL collectives and the loop-back copies are stream work and are captured
+    // with the kernels; only the host-callback backend has to run eagerly
+    const bool graphable = use_graph && sh.n == 3 && !prof && comm.kind != 2;
     const std::string key = graphable ? graph_key(order, cur, extrap, alpha, beta) : std::string();
     if (graphable && graphs.empty()) precapture(extrap, alpha, beta);
     auto it = graphable ? graphs.find(key) : graphs.end();
@@ -2193,7 +2199,23 @@ int fctn_set_comm(fctn_ctx* c, const uint8_t* id128, int rank, int nranks, int64
       if (init(&comm, nranks, id, rank) != ncclSuccess) throw std::runtime_error("ncclCommInitRank failed");
       x.comm.nccl = comm;
       x.comm.kind = 1;
+      // first collective outside any capture (NCCL sets up its channels lazily)
+      double* w = nullptr;
+      CK(cudaMalloc(&w, sizeof(double)));
+      CK(cudaMemsetAsync(w, 0, sizeof(double), x.st));
+      const ncclResult_t r = x.comm.allreduce(w, w, 1, ncclFloat64, ncclSum, comm, x.st);
+      CK(cudaStreamSynchronize(x.st));
+      cudaFree(w);
+      if (r != ncclSuccess) throw std::runtime_error("ncclAllReduce failed (warm-up)");
     }
+  });
+}
+
+int fctn_set_comm_loopback(fctn_ctx* c, int rank, int nranks, int64_t slab_lo, int64_t slab_hi) {
+  return fctn::guarded(&c->impl, [&] {
+    Ctx& x = c->impl;
+    fctn::shard_to(x, rank, nranks, slab_lo, slab_hi);
+    x.comm.kind = 3;
   });
 }
 
