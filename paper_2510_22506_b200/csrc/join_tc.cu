@@ -51,7 +51,7 @@ struct TcJoinArgs {
   int ntile;        // UMMA N (multiple of 16, <= 256)
   int pstages;
   int64_t n_mt, n_nt, ntiles, chunk;
-  bool vec_n;       // 4 consecutive n are 4 consecutive, aligned output entries
+  int vec_n;        // 4 (8): 4 (8) consecutive n are consecutive, 16-B (32-B) aligned output entries; else 0
 };
 
 struct Side {  // offsets of one operand group: index -> (operand offset, output offset)
@@ -414,7 +414,27 @@ __global__ void __launch_bounds__(NTHR, 1)
               : "=r"(o[4 * j4]), "=r"(o[4 * j4 + 1]), "=r"(o[4 * j4 + 2]), "=r"(o[4 * j4 + 3])
               : "r"(offN_s + 4 * (n0 + 4 * j4)));
         if (om >= 0) {
-          if (a.vec_n) {
+          if (a.vec_n == 8) {
+            // one full 32-byte sector per store: the 128-bit form left the SM
+            // as two half-sector writes per sector (ncu: 3.44 GB of L1 -> L2
+            // write traffic for the 1.72 GB M_k, 798 us against 484 us for
+            // the lane-coalesced form)
+#pragma unroll
+            for (int j8 = 0; j8 < 2; ++j8) {
+              if (nfull || o[8 * j8 + 7] >= 0) {
+                asm volatile("st.global.v8.f32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(Cm + o[8 * j8]),
+                             "f"(__uint_as_float(r0[8 * j8])), "f"(__uint_as_float(r0[8 * j8 + 1])),
+                             "f"(__uint_as_float(r0[8 * j8 + 2])), "f"(__uint_as_float(r0[8 * j8 + 3])),
+                             "f"(__uint_as_float(r0[8 * j8 + 4])), "f"(__uint_as_float(r0[8 * j8 + 5])),
+                             "f"(__uint_as_float(r0[8 * j8 + 6])), "f"(__uint_as_float(r0[8 * j8 + 7]))
+                             : "memory");
+              } else {
+#pragma unroll
+                for (int e = 0; e < 8; ++e)
+                  if (o[8 * j8 + e] >= 0) Cm[o[8 * j8 + e]] = __uint_as_float(r0[8 * j8 + e]);
+              }
+            }
+          } else if (a.vec_n) {
 #pragma unroll
             for (int j4 = 0; j4 < 4; ++j4) {
               if (nfull || o[4 * j4 + 3] >= 0) {
@@ -486,17 +506,21 @@ void launch_join_tc(const float* A, const float* B, float* C, const ContractDesc
   const int64_t grid = std::min<int64_t>(a.ntiles, n_sm);
   a.chunk = (a.ntiles + grid - 1) / grid;
   // n runs along the output's fastest label with unit stride (Q holds it)
-  bool vec_n = false;
-  {
+  int vec_n = 0;
+  for (int w : {8, 4}) {
     const int n = a.p_is_rows ? d.nc : d.nr;
     const int64_t* ext = a.p_is_rows ? d.c_ext : d.r_ext;
     const int64_t* sc = a.p_is_rows ? d.c_sc : d.r_sc;
-    vec_n = n >= 1 && sc[0] == 1 && ext[0] % 4 == 0 && a.ntile % 4 == 0 &&
-            reinterpret_cast<uintptr_t>(C) % 16 == 0;
-    for (int q = 1; q < n && vec_n; ++q) vec_n = sc[q] % 4 == 0;
+    bool ok = n >= 1 && sc[0] == 1 && ext[0] % w == 0 && a.ntile % w == 0 &&
+              reinterpret_cast<uintptr_t>(C) % (4 * w) == 0;
+    for (int q = 1; q < n && ok; ++q) ok = sc[q] % w == 0;
     const int np = a.p_is_rows ? d.nr : d.nc;
     const int64_t* scp = a.p_is_rows ? d.r_sc : d.c_sc;
-    for (int q = 0; q < np && vec_n; ++q) vec_n = scp[q] % 4 == 0;
+    for (int q = 0; q < np && ok; ++q) ok = scp[q] % w == 0;
+    if (ok && !(w == 8 && getenv("FCTN_JOIN_NO_V8"))) {
+      vec_n = w;
+      break;
+    }
   }
   a.vec_n = vec_n;
   const float* P = a.p_is_rows ? A : B;
