@@ -9,6 +9,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <functional>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -1595,6 +1596,19 @@ class Ctx : public Executor {
     const int cur0 = cur, mh0 = mbuf_holds;
     int64_t zv0[3] = {zver[0], zver[1], zver[2]};
     const int64_t l0 = launches;
+    struct Restore {  // also on a failed capture
+      std::function<void()> f;
+      ~Restore() { f(); }
+    } restore{[&, meter0, versions0, cur0, mh0, l0, zv0a = zv0[0], zv0b = zv0[1], zv0c = zv0[2]] {
+      planner->meter = meter0;
+      planner->versions = versions0;
+      cur = cur0;
+      zver[0] = zv0a;
+      zver[1] = zv0b;
+      zver[2] = zv0c;
+      mbuf_holds = mh0;
+      launches = l0;
+    }};
     std::vector<int> order{0, 1, 2};
     for (int parity = 0; parity < 2; ++parity) {
       do {
@@ -1621,12 +1635,6 @@ class Ctx : public Executor {
         graphs[key] = {ge, launches};
       } while (std::next_permutation(order.begin(), order.end()));
     }
-    planner->meter = meter0;
-    planner->versions = versions0;
-    cur = cur0;
-    for (int j = 0; j < 3; ++j) zver[j] = zv0[j];
-    mbuf_holds = mh0;
-    launches = l0;
   }
 
   // the host-side effects of sweep_device without any device work (graph replay)
@@ -1666,7 +1674,22 @@ class Ctx : public Executor {
     // with the kernels; only the host-callback backend has to run eagerly
     const bool graphable = use_graph && sh.n == 3 && !prof && comm.kind != 2;
     const std::string key = graphable ? graph_key(order, cur, extrap, alpha, beta) : std::string();
-    if (graphable && graphs.empty()) precapture(extrap, alpha, beta);
+    if (graphable && graphs.empty()) {
+      if (comm.kind == 1) {
+        // a communicator that cannot be captured falls back to eager sweeps
+        // (same collectives in the same order on every rank)
+        try {
+          precapture(extrap, alpha, beta);
+        } catch (const std::exception&) {
+          cudaGetLastError();
+          drop_graphs();
+          use_graph = false;
+          return sweep(order_in, extrap, alpha, beta, stats, counters);
+        }
+      } else {
+        precapture(extrap, alpha, beta);
+      }
+    }
     auto it = graphable ? graphs.find(key) : graphs.end();
     if (graphable && it != graphs.end()) {
       // replay: host bookkeeping only (the reference's FLOP meter, cache,
@@ -2199,14 +2222,18 @@ int fctn_set_comm(fctn_ctx* c, const uint8_t* id128, int rank, int nranks, int64
       if (init(&comm, nranks, id, rank) != ncclSuccess) throw std::runtime_error("ncclCommInitRank failed");
       x.comm.nccl = comm;
       x.comm.kind = 1;
-      // first collective outside any capture (NCCL sets up its channels lazily)
+      // both collectives once outside any capture (NCCL sets up its channels
+      // and buffers lazily, per collective), at a size of the sweep's own
+      // messages
+      const size_t wn = 1 << 14;
       double* w = nullptr;
-      CK(cudaMalloc(&w, sizeof(double)));
-      CK(cudaMemsetAsync(w, 0, sizeof(double), x.st));
-      const ncclResult_t r = x.comm.allreduce(w, w, 1, ncclFloat64, ncclSum, comm, x.st);
+      CK(cudaMalloc(&w, wn * (size_t)(nranks + 1) * sizeof(double)));
+      CK(cudaMemsetAsync(w, 0, wn * (size_t)(nranks + 1) * sizeof(double), x.st));
+      const ncclResult_t r1 = x.comm.allreduce(w, w, wn, ncclFloat64, ncclSum, comm, x.st);
+      const ncclResult_t r2 = x.comm.allgather(w, w + wn, wn, ncclFloat64, comm, x.st);
       CK(cudaStreamSynchronize(x.st));
       cudaFree(w);
-      if (r != ncclSuccess) throw std::runtime_error("ncclAllReduce failed (warm-up)");
+      if (r1 != ncclSuccess || r2 != ncclSuccess) throw std::runtime_error("NCCL warm-up collectives failed");
     }
   });
 }
