@@ -642,28 +642,37 @@ __global__ void __launch_bounds__(TSP_THREADS, 1)
       }
     }
   } else if (warp == 1 && lane == 0) {
-    // ---------------- MMA issuer
+    // ---------------- MMA issuer.  This one thread's instruction stream is on
+    // the critical path (a run-time switch of two branches per K step cost
+    // 12 % of the kernel), so the ring slot / phase are running counters and a
+    // stage's B descriptors are the slot-0 descriptor plus an address offset
+    // (only the 14-bit start-address field changes; shared memory < 256 KB).
     constexpr uint32_t idesc2 = tc::idesc_tf32(128, 2 * NT, false, false);
     constexpr uint32_t idesc1 = tc::idesc_tf32(128, NT, false, false);
-    int g = 0, j = 0;
+    const uint64_t bd0 = tc::sdesc(tc::smem_u32(smem) + A_BYTES, 16, 1024);
+    int s = 0, j = 0;
+    uint32_t ph = 0;
     for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++j) {
       const int acc = j % NACC;
       tc::mbar_wait(&tempty[acc], ((j / NACC) & 1) ^ 1);
       tc::fence_after_sync();
       const uint32_t d = tmem + acc * L::ACC;
-      for (int kb = 0; kb < nkb; ++kb, ++g) {
-        const int s = g % STAGES;
-        tc::mbar_wait(&conv[s], (g / STAGES) & 1);
+      for (int kb = 0; kb < nkb; ++kb) {
+        tc::mbar_wait(&conv[s], ph);
         tc::fence_after_sync();
-        const uint32_t b = tc::smem_u32(smem + s * L::STAGE_BYTES) + A_BYTES;
+        const uint64_t bds = bd0 + (uint64_t)((uint32_t)(s * L::STAGE_BYTES) >> 4);
         const uint32_t ahi = tmem + NACC * L::ACC + 64 * s, alo = ahi + 32;
 #pragma unroll
         for (int kk = 0; kk < BK / 8; ++kk) {
-          const uint64_t bd = tc::sdesc(b + kk * 32, 16, 1024);
+          const uint64_t bd = bds + (uint64_t)(2 * kk);  // + 32 bytes
           tc::mma_tf32_ts(d, ahi + 8 * kk, bd, idesc2, (kb | kk) != 0);
           tc::mma_tf32_ts(d, alo + 8 * kk, bd, idesc1, 1);
         }
         tc::mma_commit(&empty[s]);
+        if (++s == STAGES) {
+          s = 0;
+          ph ^= 1;
+        }
       }
       tc::mma_commit(&tfull[acc]);
     }
