@@ -97,6 +97,13 @@ int fctn_get_factors(fctn_ctx* ctx, double* const* a_unf);
 int fctn_get_x(fctn_ctx* ctx, void* x_F);  /* context dtype, like fctn_upload */
 int fctn_get_x_f64(fctn_ctx* ctx, double* x_F);  /* float64 whatever the context dtype */
 
+/* Closed contexts leave their large device blocks (>= 1 MB) in a process-level
+ * cache so the next context of the same extents skips cudaMalloc / cudaFree
+ * (the reference has no counterpart: numpy arrays are freed by the garbage
+ * collector, solver.py:277-399 allocates per call).  FCTN_DEVCACHE_GB bounds
+ * the idle bytes (default 16, 0 disables); this returns them to the driver. */
+int fctn_trim_cache(void);
+
 /* f(X, {A_k}) of solver.py:209-224 for the context's current X and factors
  * (full composition; used for the initial objective solver.py:302 and the
  * rank-growth continuity test solver.py:416).  Adds the compose FLOPs of the

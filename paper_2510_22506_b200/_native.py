@@ -8,6 +8,7 @@ from __future__ import annotations
 
 import ctypes as C
 import os
+import threading
 
 import numpy as np
 
@@ -25,7 +26,7 @@ EXPORTS = [
     "fctn_create", "fctn_upload", "fctn_upload_f64", "fctn_get_x_f64", "fctn_set_factors", "fctn_set_rank", "fctn_get_factors", "fctn_get_x",
     "fctn_objective", "fctn_sweep", "fctn_plan_sweeps", "fctn_nccl_unique_id", "fctn_set_comm", "fctn_set_comm_host", "fctn_set_comm_loopback",
     "fctn_sync", "fctn_selftest_stream", "fctn_selftest_chol", "fctn_selftest_eigh", "fctn_timer", "fctn_set_profiling", "fctn_get_profile", "fctn_last_error", "fctn_version",
-    "fctn_quality", "fctn_quality_ctx", "fctn_destroy",
+    "fctn_quality", "fctn_quality_ctx", "fctn_destroy", "fctn_trim_cache",
 ]
 Q_PSNR, Q_SSIM, Q_ERR_SQ, Q_REF_SQ, Q_OFF_ERR_SQ, Q_OFF_REF_SQ, Q_OFF_COUNT, Q_COUNT = 0, 1, 2, 3, 4, 5, 6, 8
 K_CLASSES = ["merge", "stream_y", "gram", "reduce", "chol", "compose", "dft", "fgram", "zpass", "ysmall", "mbuild",
@@ -37,21 +38,89 @@ HOST_ALLREDUCE = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_double), C.c_int
 HOST_ALLGATHER = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_double), C.c_int64)
 
 
+class _HostBlock:
+    """An anonymous mapping (advised for transparent huge pages) that exports
+    its bytes (PEP 688) and goes back to the pool when the last array or view
+    over it is gone, so a later download of the same size finds its pages
+    already faulted in."""
+
+    def __init__(self, mm, nbytes):
+        self.mm, self.nbytes = mm, nbytes
+
+    def __buffer__(self, flags):
+        return memoryview(self.mm)
+
+    def __release_buffer__(self, view):
+        view.release()
+
+    def __del__(self):
+        try:
+            _host_pool_put(self.mm, self.nbytes)
+        except Exception:  # interpreter shutdown
+            pass
+
+
+_HOST_POOL = {}  # nbytes -> [mmap, ...]
+_HOST_POOL_IDLE = [0]
+_HOST_POOL_LOCK = threading.Lock()
+
+
+def _host_pool_cap() -> int:
+    return int(float(os.environ.get("FCTN_HOSTPOOL_GB", "8")) * (1 << 30))
+
+
+def _host_pool_put(mm, nbytes):
+    with _HOST_POOL_LOCK:
+        if _HOST_POOL_IDLE[0] + nbytes <= _host_pool_cap():
+            _HOST_POOL.setdefault(nbytes, []).append(mm)
+            _HOST_POOL_IDLE[0] += nbytes
+            return
+    mm.close()
+
+
+def trim_host_pool():
+    """Unmap every idle download buffer."""
+    with _HOST_POOL_LOCK:
+        for blocks in _HOST_POOL.values():
+            for mm in blocks:
+                mm.close()
+        _HOST_POOL.clear()
+        _HOST_POOL_IDLE[0] = 0
+
+
+def trim_cache():
+    """Return the idle device blocks of closed contexts to the driver
+    (fctn_trim_cache) and unmap the idle host download buffers."""
+    lib().fctn_trim_cache()
+    trim_host_pool()
+
+
 def _host_empty(dims) -> np.ndarray:
-    """F-order float64 array for a large download: backed by an anonymous
-    mapping advised for transparent huge pages, so first-touch page faults
-    during the device->host copy are ~512x fewer."""
+    """F-order float64 array for a large download.  The first-touch page
+    faults of a fresh 2 GB array cost as much as the transfer (and several
+    times more when the kernel has no huge pages to give), so large results
+    live in pooled anonymous mappings: the block returns to the pool when the
+    caller drops the array (and every view of it), and the next download of
+    that size reuses the faulted pages.  FCTN_HOSTPOOL_GB bounds the idle
+    bytes (default 8, 0 disables pooling)."""
     n = int(np.prod(dims))
     nbytes = n * 8
     if nbytes < (64 << 20):
         return np.empty(dims, dtype=np.float64, order="F")
     import mmap
-    buf = mmap.mmap(-1, nbytes, flags=mmap.MAP_PRIVATE | mmap.MAP_ANONYMOUS)
-    try:
-        buf.madvise(mmap.MADV_HUGEPAGE)
-    except (AttributeError, OSError):
-        pass
-    return np.frombuffer(buf, dtype=np.float64, count=n).reshape(dims, order="F")
+    mm = None
+    with _HOST_POOL_LOCK:
+        blocks = _HOST_POOL.get(nbytes)
+        if blocks:
+            mm = blocks.pop()
+            _HOST_POOL_IDLE[0] -= nbytes
+    if mm is None:
+        mm = mmap.mmap(-1, nbytes, flags=mmap.MAP_PRIVATE | mmap.MAP_ANONYMOUS)
+        try:
+            mm.madvise(mmap.MADV_HUGEPAGE)
+        except (AttributeError, OSError):
+            pass
+    return np.frombuffer(_HostBlock(mm, nbytes), dtype=np.float64, count=n).reshape(dims, order="F")
 
 
 def slab_of(I0: int, rank: int, nranks: int):

@@ -46,6 +46,82 @@ struct CudaError : std::runtime_error {
       throw ::fctn::CudaError(std::string(#call) + " failed: " + cudaGetErrorString(_e));            \
   } while (0)
 
+// Process-level cache of the large device blocks (>= 1 MB) a context owns:
+// cudaMalloc / cudaFree of a few GB cost ~90 ms per create + close pair, a
+// third of a short run(obs, cfg) call.  A closed context's blocks stay idle
+// here (up to FCTN_DEVCACHE_GB, default 16; 0 disables) and the next context
+// with the same extents takes them back by exact size; an allocation failure
+// or fctn_trim_cache() returns them to the driver.  Contents are stale, as
+// with any cudaMalloc.
+struct DevCache {
+  static constexpr size_t MIN_BYTES = (size_t)1 << 20;
+  std::mutex mu;
+  std::multimap<std::pair<int, size_t>, void*> idle;
+  std::map<void*, std::pair<int, size_t>> live;
+  size_t idle_bytes = 0, cap = 0;
+  DevCache() {
+    const char* e = getenv("FCTN_DEVCACHE_GB");
+    cap = (size_t)((e ? atof(e) : 16.0) * (double)(1ull << 30));
+  }
+  cudaError_t alloc(void** p, size_t n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const bool cached = cap > 0 && n >= MIN_BYTES;
+    if (cached) {
+      std::lock_guard<std::mutex> g(mu);
+      auto it = idle.find({dev, n});
+      if (it != idle.end()) {
+        *p = it->second;
+        idle.erase(it);
+        idle_bytes -= n;
+        live[*p] = {dev, n};
+        return cudaSuccess;
+      }
+    }
+    cudaError_t e = cudaMalloc(p, n);
+    if (e == cudaErrorMemoryAllocation && idle_bytes > 0) {
+      cudaGetLastError();
+      trim();
+      e = cudaMalloc(p, n);
+    }
+    if (e == cudaSuccess && cached) {
+      std::lock_guard<std::mutex> g(mu);
+      live[*p] = {dev, n};
+    }
+    return e;
+  }
+  cudaError_t release(void* p) {
+    if (!p) return cudaSuccess;
+    {
+      std::lock_guard<std::mutex> g(mu);
+      auto it = live.find(p);
+      if (it != live.end()) {
+        const std::pair<int, size_t> key = it->second;
+        live.erase(it);
+        if (idle_bytes + key.second <= cap) {
+          idle.insert({key, p});
+          idle_bytes += key.second;
+          return cudaSuccess;
+        }
+      }
+    }
+    return cudaFree(p);
+  }
+  void trim() {
+    std::lock_guard<std::mutex> g(mu);
+    for (auto& kv : idle) cudaFree(kv.second);
+    idle.clear();
+    idle_bytes = 0;
+  }
+};
+static DevCache& dev_cache() {
+  static DevCache* c = new DevCache();  // never destroyed: contexts may outlive static destruction order
+  return *c;
+}
+// every cudaMalloc / cudaFree below this line goes through the cache
+#define cudaMalloc(p, n) ::fctn::dev_cache().alloc((void**)(p), (size_t)(n))
+#define cudaFree(p) ::fctn::dev_cache().release((void*)(p))
+
 static const int64_t M_ID = 0;    // fixed executor id of the M_k buffer
 static const int64_t X_ID = -10;  // the current iterate X (labels 0 .. n-1, first fastest)
 static const int64_t Y_ID = -11;  // the fp64 Y_k buffer (labels [k, bonds to k])
@@ -2012,6 +2088,11 @@ int fctn_upload_f64(fctn_ctx* c, const double* x_F, const uint8_t* mask_F) {
     x.z_invalidate();
     x.mbuf_holds = -1;
   });
+}
+
+int fctn_trim_cache(void) {
+  fctn::dev_cache().trim();
+  return 0;
 }
 
 int fctn_get_x_f64(fctn_ctx* c, double* x_F) {

@@ -264,3 +264,34 @@ def test_gpu_other_associations_match_reference(monkeypatch, name, dtype):
     for i, r in enumerate(res.trace):
         assert (r.flops, r.mk_flops, r.cache_hits) == (case["trace_flops"][i], case["trace_mk_flops"][i],
                                                       case["trace_cache_hits"][i])
+
+
+def test_gpu_cached_blocks_and_pooled_download_reuse():
+    """Closed contexts leave their device blocks in the process-level cache and
+    a dropped result returns its download buffer to the host pool: a second
+    and a third run (after trimming both) give the bits of the first."""
+    import gc
+
+    from paper_2510_22506_b200 import _native
+
+    wl, truth, mask = make_instance("c4", dims=(512, 256, 64))  # X as float64: 67 MB, pooled (>= 64 MB)
+    kw = dict(lam=0.35, delta=0.5, rho=0.1, eps=0.0, max_iters=3, max_rank=4, initial_rank=4,
+              rank_policy="fixed", algorithm="afctnlr", shuffle=True, seed=0)
+    obs = P.Observation(truth, mask)
+    a = P.run(obs, P.SolverConfig(**kw), dtype="float32")
+    xa = a.x.copy()
+    view = a.x[:3]
+    del a
+    gc.collect()
+    idle0 = _native._HOST_POOL_IDLE[0]  # the view keeps the block out of the pool
+    del view
+    gc.collect()
+    assert _native._HOST_POOL_IDLE[0] == idle0 + xa.nbytes
+    b = P.run(obs, P.SolverConfig(**kw), dtype="float32")  # reuses device blocks and the host block
+    assert np.array_equal(b.x, xa)
+    del b
+    gc.collect()
+    _native.trim_cache()
+    assert _native._HOST_POOL_IDLE[0] == 0
+    c = P.run(obs, P.SolverConfig(**kw), dtype="float32")
+    assert np.array_equal(c.x, xa)
