@@ -1999,6 +1999,69 @@ struct Stager {
     }
     CK(cudaStreamSynchronize(st));
   }
+  // f(lo, hi) over [0, n) on the copy threads
+  template <typename F>
+  void pfor(size_t n, F&& f) const {
+    if (nthr <= 1 || n < ((size_t)1 << 20)) {
+      f((size_t)0, n);
+      return;
+    }
+    const size_t part = ((n + nthr - 1) / nthr + 1023) & ~(size_t)1023;
+    std::vector<std::thread> th;
+    for (int t = 1; t < nthr; ++t) {
+      const size_t o = (size_t)t * part;
+      if (o >= n) break;
+      th.emplace_back([=] { f(o, std::min(n, o + part)); });
+    }
+    f((size_t)0, std::min(part, n));
+    for (auto& x : th) x.join();
+  }
+  // fp64 host tensor -> fp32 device tensor: the copy threads round to fp32
+  // (round-to-nearest-even, the bits of the device's own conversion) while
+  // they fill the pinned ring, so half the bytes cross PCIe and the ring
+  void h2d_f64_to_f32(float* dst, const double* src, size_t count, cudaStream_t st) {
+    const size_t CE = CH / 4;  // floats per ring buffer
+    size_t c = 0;
+    for (size_t o = 0; o < count; o += CE, ++c) {
+      const int b = (int)(c % NB);
+      const size_t m = std::min(CE, count - o);
+      CK(cudaEventSynchronize(ev[b]));
+      float* stage = (float*)buf[b];
+      const double* from = src + o;
+      pfor(m, [=](size_t lo, size_t hi) {
+        for (size_t e = lo; e < hi; ++e) stage[e] = (float)from[e];
+      });
+      CK(cudaMemcpyAsync(dst + o, stage, m * 4, cudaMemcpyHostToDevice, st));
+      CK(cudaEventRecord(ev[b], st));
+    }
+    CK(cudaStreamSynchronize(st));
+  }
+  // fp32 device tensor -> fp64 host tensor, widened by the copy threads
+  void d2h_f32_to_f64(double* dst, const float* src, size_t count, cudaStream_t st) {
+    const size_t CE = CH / 4;
+    const size_t nc = (count + CE - 1) / CE;
+    for (size_t c = 0; c <= nc; ++c) {
+      if (c < nc) {
+        const int b = (int)(c % NB);
+        const size_t o = c * CE, m = std::min(CE, count - o);
+        CK(cudaEventSynchronize(ev[b]));
+        CK(cudaMemcpyAsync(buf[b], src + o, m * 4, cudaMemcpyDeviceToHost, st));
+        CK(cudaEventRecord(ev[b], st));
+      }
+      if (c >= 1) {
+        const size_t pc = c - 1;
+        const int pb = (int)(pc % NB);
+        const size_t o = pc * CE, m = std::min(CE, count - o);
+        CK(cudaEventSynchronize(ev[pb]));
+        const float* stage = (const float*)buf[pb];
+        double* to = dst + o;
+        pfor(m, [=](size_t lo, size_t hi) {
+          for (size_t e = lo; e < hi; ++e) to[e] = (double)stage[e];
+        });
+      }
+    }
+    CK(cudaStreamSynchronize(st));
+  }
   // D2H of n bytes produced chunk by chunk: `produce(o, m)` enqueues on `st`
   // whatever must run before chunk [o, o+m) of `src` is ready (may be empty)
   template <typename Produce>
@@ -2080,7 +2143,9 @@ int fctn_upload_f64(fctn_ctx* c, const double* x_F, const uint8_t* mask_F) {
     if (x.dtype == FCTN_F64) {
       if (stage) fctn::stager()->h2d(x.X[0], x_F, (size_t)T * 8, x.st);
       else CK(cudaMemcpyAsync(x.X[0], x_F, T * 8, cudaMemcpyHostToDevice, x.st));
-    } else {  // fp64 host data, fp32 context: convert on the device, in chunks
+    } else if (stage) {  // fp64 host data, fp32 context: rounded by the ring's copy threads
+      fctn::stager()->h2d_f64_to_f32((float*)x.X[0], x_F, (size_t)T, x.st);
+    } else {  // small tensors: convert on the device, in chunks
       const int64_t chunk = std::min<int64_t>(T, (int64_t)1 << 26);
       fctn::DevScratch scratch(chunk * 8, x.st);
       double* tmp = (double*)scratch.p;
@@ -2116,30 +2181,8 @@ int fctn_get_x_f64(fctn_ctx* c, double* x_F) {
       fctn::Stager& sg = *lease.s;
       if (x.dtype == FCTN_F64) {
         sg.d2h(x_F, x.X[x.cur], (size_t)T * 8, x.st, [](size_t, size_t, int) {});
-      } else {  // convert each 32 MB chunk on the device into one of three scratch slots
-        const size_t cd = fctn::Stager::CH / 8;  // doubles per chunk
-        fctn::DevScratch tmp(3 * fctn::Stager::CH, x.st);
-        const float* X32 = (const float*)x.X[x.cur];
-        // explicit pipeline: chunk c is converted into scratch slot c % 3 and read from there
-        const size_t n = (size_t)T * 8;
-        const size_t nc = (n + fctn::Stager::CH - 1) / fctn::Stager::CH;
-        for (size_t ci = 0; ci <= nc; ++ci) {
-          if (ci < nc) {
-            const int b = (int)(ci % fctn::Stager::NB);
-            const size_t off = ci * fctn::Stager::CH, m = std::min(fctn::Stager::CH, n - off);
-            double* slot = (double*)tmp.p + (size_t)b * cd;
-            fctn::launch_convert_f32_f64(X32 + off / 8, slot, (int64_t)(m / 8), x.st);
-            CK(cudaMemcpyAsync(sg.buf[b], slot, m, cudaMemcpyDeviceToHost, x.st));
-            CK(cudaEventRecord(sg.ev[b], x.st));
-          }
-          if (ci >= 1) {
-            const size_t pc = ci - 1;
-            const int pb = (int)(pc % fctn::Stager::NB);
-            const size_t off = pc * fctn::Stager::CH, m = std::min(fctn::Stager::CH, n - off);
-            CK(cudaEventSynchronize(sg.ev[pb]));
-            sg.pcopy((char*)x_F + off, sg.buf[pb], m);
-          }
-        }
+      } else {  // fp32 over PCIe, widened to fp64 by the ring's copy threads
+        sg.d2h_f32_to_f64(x_F, (const float*)x.X[x.cur], (size_t)T, x.st);
       }
       CK(cudaStreamSynchronize(x.st));
       return;

@@ -29,3 +29,28 @@ cfg = P.SolverConfig(max_iters=20, max_rank=wl.rank, initial_rank=wl.rank, lam=0
                      rank_policy="fixed", algorithm="afctnlr", shuffle=True, seed=0)
 res = P.run(obs, cfg, dtype="float32" if dt == _native.F32 else "float64")
 print("run() total ms", round((time.perf_counter() - t0) * 1e3, 1))
+
+# ---- six more run() calls with the context methods timed (which phase varies call to call?)
+import gc
+acc = {}
+def _wrap(cls, name):
+    f = getattr(cls, name)
+    def g(self, *a, **k):
+        t = time.perf_counter()
+        try:
+            return f(self, *a, **k)
+        finally:
+            acc[name] = acc.get(name, 0.0) + (time.perf_counter() - t) * 1e3
+    setattr(cls, name, g)
+for nm in ("__init__", "upload_f64", "set_factors", "sweep", "objective", "get_x_f64", "get_factors", "close"):
+    _wrap(_native.Context, nm)
+del res
+for i in range(6):
+    acc.clear()
+    gc.collect()
+    t0 = time.perf_counter()
+    res = P.run(obs, cfg, dtype="float32" if dt == _native.F32 else "float64")
+    tot = (time.perf_counter() - t0) * 1e3
+    print("run", i, "total", round(tot, 1), {k: round(v, 1) for k, v in acc.items()},
+          "other", round(tot - sum(acc.values()), 1), "pool idle", _native._HOST_POOL_IDLE[0] >> 20, "MB")
+    del res

@@ -25,4 +25,4 @@ full c4_chol c4 "k_chol" 6
 full c5_join c5 "k_join_tc" 4
 full c5_stream c5 "k_stream_tsw" 2
 full c5_compose c5 "k_compose" 1
-full c3_stream c3 "k_stream<" 4
+full c3_stream c3 "k_stream_dmma" 4

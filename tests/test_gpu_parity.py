@@ -221,6 +221,9 @@ def test_gpu_solve_forms_match_reference_golden(monkeypatch, name, solve):
     ((8192, 6, 5), 2, 6),       # I_0 = 8192 > 4266: the long-mode DFT from global scratch
     ((5000, 7, 3), 3, 4),       # long mode with a non-power-of-two extent
     ((8, 7, 6, 5), 6, 4),       # N = 4, R = 6: s = 216 > 160, the global-memory Jacobi solve
+    ((64, 32, 16), 3, 6),       # power-of-two extents: the radix-2 shared-memory FFT, even stage counts
+    ((8, 128, 512), 2, 5),      # ... odd stage counts (result in the second buffer pair), I = 8 the smallest
+    ((4096, 4, 2), 2, 4),       # ... the longest on-chip power of two (12 stages)
 ])
 def test_gpu_general_sizes_match_oracle(dims, rank, iters):
     """Inputs beyond the on-chip limits the reference also accepts
