@@ -435,8 +435,11 @@ def run_ours(args, wl, name):
     T = wl.total
     fac_bytes = sum(8 * wl.dims[k] * wl.rank ** (n - 1) for k in range(n))
     e2e = {"value": round(n_iter / t_e2e, 4), "unit": UNIT,
-           "h2d_bytes_per_step": int((T * 8 + T + fac_bytes) / n_iter),  # fp64 values + mask bytes
-           "d2h_bytes_per_step": int((T * 8 + fac_bytes) / n_iter),      # fp64 X + factors
+           # bytes that cross PCIe: the caller's fp64 tensor is rounded to the context dtype by the
+           # staging ring's copy threads (and widened again on the way back), + mask bytes, + fp64 factors
+           "h2d_bytes_per_step": int((T * b + T + fac_bytes) / n_iter),
+           "d2h_bytes_per_step": int((T * b + fac_bytes) / n_iter),
+           "host_tensor_bytes": int(T * 8),
            "run_s": [round(v, 4) for v in t_runs],
            "note": "median of 3 run(obs, cfg) calls: context + upload + K sweeps + download each, bytes "
                    "amortised per sweep"}
