@@ -1963,7 +1963,9 @@ struct Stager {
       CK(cudaEventCreateWithFlags(&ev[b], cudaEventDisableTiming));
     }
     const unsigned hc = std::thread::hardware_concurrency();
-    nthr = (int)std::max(1u, std::min(8u, hc ? hc / 2 : 1u));
+    // one copy thread per host core up to 16 (measured with the fp64 <-> fp32
+    // conversion on these threads: 8 -> 16 threads, upload 54 -> 43 ms, download 64 -> 46 ms at c4)
+    nthr = (int)std::max(1u, std::min(16u, hc ? hc : 1u));
     if (const char* e = getenv("FCTN_STAGE_THREADS")) nthr = std::max(1, atoi(e));
   }
   ~Stager() {

@@ -47,7 +47,13 @@ def test_stream_fp64_matches_numpy(dims, k, S):
     assert np.linalg.norm(y - ref) / np.linalg.norm(ref) <= 1e-13
 
 
-@pytest.mark.parametrize("S,H1", [(16, 129), (36, 129), (64, 1025), (81, 25), (125, 89)])
+@pytest.mark.parametrize("S,H1", [
+    (16, 129), (36, 129), (64, 1025), (81, 25), (125, 89),
+    (64, 33),    # 32 x 32 threads, TL = 2, s = SP: the unchecked substitution steps
+    (48, 300),   # 16 x 16 threads, TL = 3, s = SP
+    (100, 200),  # 16 x 16 threads, TL = 7: per-column barriers instead of panels
+    (150, 40),   # 32 x 32 threads, TL = 5
+])
 def test_chol_solves_match_numpy(S, H1):
     rng = np.random.default_rng(S)
     Mk = rng.standard_normal((S, 4 * S))
