@@ -242,7 +242,7 @@ class Ctx : public Executor {
   int form_for(int k, bool long_y) const {
     (void)long_y;
     const int64_t S = gsh.s_of(k);
-    if (S > 160) return FORM_EIGH;
+    if (S > 160 || !chol_solve_fits(S)) return FORM_EIGH;  // (the Cholesky CTA holds s <= 146)
     if (solve_pref == 2) return eigh_fits_smem(S) ? FORM_EIGH : FORM_CHOL;
     if (solve_pref == 3) return tridiag_fits_smem(S) ? FORM_TRI : FORM_CHOL;
     return FORM_CHOL;

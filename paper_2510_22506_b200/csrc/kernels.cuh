@@ -123,6 +123,7 @@ void launch_dft_fwd(const double* Y, const DftPlan& p, int64_t S, const double* 
                     double* Fr, double* Fi, cudaStream_t st, double* gscr = nullptr);
 // per-frequency Cholesky solves of (G + mu_w I) a_w = F_w; extra check CTA
 // when check_mu is finite (T-floor test, sylvester.py:108-113)
+bool chol_solve_fits(int64_t S);  // one system's factor + panel buffers fit shared memory (s <= 146)
 void launch_chol_solve(const double* G, int64_t S, int64_t H1, const double* mu, double* Fr, double* Fi,
                        double check_mu, int* status, cudaStream_t st);
 // inverse DFT + extrapolation + factor write + per-column stats

@@ -52,7 +52,7 @@ def test_stream_fp64_matches_numpy(dims, k, S):
     (64, 33),    # 32 x 32 threads, TL = 2, s = SP: the unchecked substitution steps
     (48, 300),   # 16 x 16 threads, TL = 3, s = SP
     (100, 200),  # 16 x 16 threads, TL = 7: per-column barriers instead of panels
-    (150, 40),   # 32 x 32 threads, TL = 5
+    (144, 40),   # 32 x 32 threads, TL = 5 (s <= 146 fits the CTA's shared memory)
 ])
 def test_chol_solves_match_numpy(S, H1):
     rng = np.random.default_rng(S)

@@ -224,6 +224,8 @@ def test_gpu_solve_forms_match_reference_golden(monkeypatch, name, solve):
     ((64, 32, 16), 3, 6),       # power-of-two extents: the radix-2 shared-memory FFT, even stage counts
     ((8, 128, 512), 2, 5),      # ... odd stage counts (result in the second buffer pair), I = 8 the smallest
     ((4096, 4, 2), 2, 4),       # ... the longest on-chip power of two (12 stages)
+    ((40, 12, 9), (10, 15, 2), 4),  # s_0 = 150: above the Cholesky CTA's 146, below 160 -> eigenbasis form
+    ((30, 14, 9), (12, 12, 2), 4),  # s_0 = 144: the largest Cholesky systems (32 x 32 threads, TL = 5)
 ])
 def test_gpu_general_sizes_match_oracle(dims, rank, iters):
     """Inputs beyond the on-chip limits the reference also accepts
