@@ -8,6 +8,7 @@ from __future__ import annotations
 
 import ctypes as C
 import os
+import sys
 import threading
 
 import numpy as np
@@ -120,6 +121,8 @@ def _host_empty(dims) -> np.ndarray:
             mm.madvise(mmap.MADV_HUGEPAGE)
         except (AttributeError, OSError):
             pass
+    if sys.version_info < (3, 12):  # no __buffer__ protocol for Python classes: unpooled mapping
+        return np.frombuffer(mm, dtype=np.float64, count=n).reshape(dims, order="F")
     return np.frombuffer(_HostBlock(mm, nbytes), dtype=np.float64, count=n).reshape(dims, order="F")
 
 

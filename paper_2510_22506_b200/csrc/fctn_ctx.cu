@@ -221,15 +221,15 @@ class Ctx : public Executor {
   // Which form solves update k.  The eigenbasis form (eigh.cu, the
   // reference's own) runs on a side stream concurrently with the Y_k pass, so
   // it is off the critical path when its single-SM Jacobi is shorter than
-  // that pass.  s > 160 has no Cholesky kernel: always eigh (from global
-  // memory above s = 117).  The choice depends only on global shapes and the
+  // that pass.  s > 146 has no Cholesky kernel (one system no longer fits a
+  // CTA's shared memory): always eigh (from global memory above s = 117).  The choice depends only on global shapes and the
   // visiting order, so every rank of a sharded run makes the same one.
   //
   // Three exact forms:
   //   chol (solve.cu) per-frequency Cholesky of G + mu_w I over all SMs --
-  //                   the default for s <= 160;
+  //                   the default for s <= 146;
   //   eigh (eigh.cu)  Jacobi eigendecomposition G = V diag(phi) V^T, the
-  //                   reference's literal form: s > 160 (from global memory)
+  //                   reference's literal form: s > 146 (from global memory)
   //                   or FCTN_SOLVE=eigh;
   //   tri  (tri.cu)   G = Q T Q^T, per-frequency tridiagonal solves
   //                   (FCTN_SOLVE=tri).
