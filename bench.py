@@ -441,8 +441,10 @@ def run_ours(args, wl, name):
            "d2h_bytes_per_step": int((T * b + fac_bytes) / n_iter),
            "host_tensor_bytes": int(T * 8),
            "run_s": [round(v, 4) for v in t_runs],
-           "note": "median of 3 run(obs, cfg) calls: context + upload + K sweeps + download each, bytes "
-                   "amortised per sweep"}
+           "note": "median of 3 run(obs, cfg) calls in one process: context + upload + K sweeps + download "
+                   "each, bytes amortised per sweep; the first call allocates device memory and faults in the "
+                   "result array, later calls reuse the library's device-block cache and pooled download "
+                   "buffer (run_s lists all three)"}
 
     cpu = None
     if ws == 1 and not args.no_cpu_baseline:
